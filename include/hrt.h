@@ -1,0 +1,183 @@
+/*
+ * hrt.h - C ABI of the B200-native hybrid NeRF/mesh renderer (libhrt.so).
+ *
+ * Drop-in boundary for the reference render path (arxiv 2309.04581
+ * reference package `hybridrt`, pure Python). The reference has no FFI; its
+ * seams are Python duck types, and each entry point below replaces one of
+ * them (reference file:line under pkg/src/hybridrt/):
+ *
+ *   hrt_create / hrt_destroy  <- scene assembly build_scene + Bvh(...)       scene.py:502-554, surface.py:289-369
+ *   hrt_render               <- render / render_surface_only /
+ *                               render_volume_only (mode 0/1/2)              render.py:372-396
+ *   hrt_render_host          <- same, host buffers in/out (what `render`
+ *                               returns: HdrImage pixels)                    render.py:353-369
+ *   hrt_trace_paths          <- trace_path (batch of caller rays)            render.py:302-312
+ *   hrt_refit                <- Scene.rebuild_bvh after sim sync             scene.py:475-479, sim.py:673-698
+ *   hrt_field_sample         <- field seam field.sample_batch(p[, d])       field.py:143-161
+ *   hrt_field_encode         <- (new) hash-grid encode, parity probe
+ *   hrt_occupancy            <- (new) occupancy bitfield readback
+ *   hrt_intersect            <- Bvh.intersect_batch / any_hit_batch          surface.py:377-478
+ *   hrt_uniform              <- rng.uniform                                  rng.py:54-57
+ *   hrt_primary_rays         <- _sample_jitter + Camera.primary_rays         render.py:61-74, 320-330
+ *
+ * Conventions (reference render.py:245, 368, 378; scene.py:27-32):
+ *   return 0 on success; HRT_EINVAL -> ValueError, HRT_ENONFINITE ->
+ *   AssertionError (NaN / negative radiance), HRT_ECUDA / HRT_ENOMEM ->
+ *   RuntimeError. hrt_last_error() describes the last failure (thread-local).
+ * Memory: every pointer in hrt_scene_desc is a HOST pointer, copied during
+ *   hrt_create (the library owns its device copies and scratch queues).
+ *   Pointers marked "device" in the probes are device pointers on the
+ *   handle's device. `stream` is a cudaStream_t (NULL = default stream).
+ * Threading: calls on one handle are serialised by the caller; one handle
+ *   per device.
+ */
+#ifndef HRT_H
+#define HRT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HRT_OK 0
+#define HRT_EINVAL 1
+#define HRT_ENONFINITE 2
+#define HRT_ECUDA 3
+#define HRT_ENOMEM 4
+
+#define HRT_FIELD_NONE 0
+#define HRT_FIELD_DENSE 1
+#define HRT_FIELD_NEURAL 2
+
+#define HRT_MODE_HYBRID 0
+#define HRT_MODE_SURFACE 1
+#define HRT_MODE_VOLUME 2
+
+typedef struct hrt_handle hrt_handle;
+
+typedef struct {
+    int32_t kind;                 /* HRT_FIELD_* */
+    int32_t identity;             /* world_from_field is the identity */
+    double bbox_lo[3], bbox_hi[3];
+    double field_from_world[16];  /* row-major 4x4 inverse placement */
+    /* dense RadianceGrid (field.py:104-175) */
+    int32_t res[3];
+    double scale[3];              /* (res-1)/(hi-lo), 0 where res == 1 */
+    const double* sigma;          /* nx*ny*nz, C order (z fastest) */
+    const double* radiance;       /* nx*ny*nz*3 */
+    int32_t sigma_const, rad_const;
+    /* neural field */
+    int32_t n_levels, n_features, log2_table, act;   /* act 0 sigmoid, 1 softplus */
+    const int32_t* level_n;       /* N_l */
+    const int64_t* level_offset;  /* entry offset per level */
+    const int32_t* level_dense;
+    const float* level_scale;     /* L x 3 float32 N_l / (hi - lo) */
+    const float* table;           /* n_entries x n_features */
+    int64_t n_entries;
+    const uint16_t* w_density1;   /* fp16 bits, row-major [in][out]: (L*F) x 64 */
+    const uint16_t* w_density2;   /* 64 x 16 */
+    const uint16_t* w_color1;     /* 32 x 64 */
+    const uint16_t* w_color2;     /* 64 x 64 */
+    const uint16_t* w_color3;     /* 64 x 3 */
+    int32_t occ_res;
+    float occ_scale[3];           /* float32 G / (hi - lo) */
+    double occ_threshold;
+    const uint32_t* occ_bits;     /* NULL: built on the device from density */
+} hrt_field_desc;
+
+typedef struct {
+    int64_t n_faces;              /* meshes concatenated in scene order */
+    const double* v0;             /* n_faces x 3 */
+    const double* e1;             /* v1 - v0 */
+    const double* e2;             /* v2 - v0 */
+    const double* normal;         /* unit face normals */
+    const double* emission;       /* n_faces x 3 */
+    const int32_t* mesh_of;       /* face -> mesh (material) index */
+    int32_t n_materials;
+    const int32_t* mat_kind;      /* 0 Lambertian, 1 Mirror, 2 Dielectric */
+    const double* mat_rgb;        /* albedo / reflectance / tint, n_materials x 3 */
+    const double* mat_ior;
+    int64_t n_blockers;           /* non-emissive faces (shadow rays) */
+    const double *bv0, *be1, *be2;
+    int32_t n_emitters;
+    const double* emitter_tris;   /* n x 9 */
+    const double* emitter_cdf;
+    const double* emitter_rsrc;
+    hrt_field_desc field;
+    int32_t n_bounces;
+    double threshold, march_step, spawn_eps;
+    int32_t sample_cap;           /* NeRF samples per path, 0 = unlimited */
+    double early_t;               /* in-march early-out on max(T_spec), 0 = off */
+} hrt_scene_desc;
+
+typedef struct {
+    double rot[9];                /* camera-to-world rotation (pose.m[:3,:3]) */
+    double pos[3];
+    double tan_half;              /* tan(fov / 2), vertical fov */
+    double aspect;                /* width / height */
+    int32_t width, height;
+} hrt_camera;
+
+typedef struct {
+    int64_t paths;
+    int64_t nerf_samples;         /* encode + MLP evaluations */
+    int64_t shadow_rays;
+    int64_t bounce_rays;          /* closest-hit queries */
+    int64_t trace_records;
+    float ms;                     /* device time of the call */
+} hrt_stats;
+
+const char* hrt_last_error(void);
+int hrt_version(void);
+
+int hrt_create(const hrt_scene_desc* desc, hrt_handle** out);
+int hrt_destroy(hrt_handle* h);
+
+/* Render n_pixels listed pixel ids (device int32, NULL = all w*h in raster
+ * order) x spp paths. out: device, n_pixels x 3 float64 linear radiance. */
+int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed, int32_t mode,
+               const int32_t* pixels, int64_t n_pixels, double* out, hrt_stats* stats,
+               void* stream);
+
+/* Same with host pixels / host out; copies inside, synchronous. */
+int hrt_render_host(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
+                    int32_t mode, const int32_t* pixels, int64_t n_pixels, double* out,
+                    hrt_stats* stats);
+
+/* Caller-supplied rays (device o, d: n x 3; pixel/sample keys int64) through
+ * the same bounce loop; L: device n x 3 (trace_path, render.py:302-312). */
+int hrt_trace_paths(hrt_handle* h, const double* o, const double* d, const int64_t* pixel,
+                    const int64_t* sample, int64_t n, uint64_t seed, int32_t mode, double* L,
+                    void* stream);
+
+/* Debug trace of evaluated NeRF samples: int32 records (path, bounce, k,
+ * occupancy cell) in device memory, up to cap records; enabled for the
+ * next hrt_render call only. */
+int hrt_set_trace(hrt_handle* h, int32_t* records, int64_t cap);
+
+/* New world-space face geometry (same topology; host pointers). */
+int hrt_refit(hrt_handle* h, const double* v0, const double* e1, const double* e2,
+              const double* normal, const double* bv0, const double* be1, const double* be2);
+
+/* Field seam probes (device pointers). dirs may be NULL (density only). */
+int hrt_field_sample(hrt_handle* h, const double* points, const double* dirs, int64_t n,
+                     float* sigma, float* rgb, int32_t* evaluated, int32_t use_occupancy,
+                     void* stream);
+int hrt_field_encode(hrt_handle* h, const double* points, int64_t n, float* features,
+                     uint32_t* indices, void* stream);
+int hrt_occupancy(hrt_handle* h, uint32_t* host_words, int64_t n_words);
+
+/* Geometry / RNG / camera probes (device pointers). blocker: 0 scene BVH,
+ * 1 shadow blockers. any: 0 nearest (t, face), 1 any-hit (hit). */
+int hrt_intersect(hrt_handle* h, int32_t blocker, int32_t any, const double* o, const double* d,
+                  const double* t_min, const double* t_max, int64_t n, double* t, int64_t* face,
+                  uint8_t* hit, void* stream);
+int hrt_uniform(const int64_t* keys, int64_t n, double* out, void* stream);
+int hrt_primary_rays(const hrt_camera* cam, const int64_t* pixel, const int64_t* sample,
+                     int64_t n, uint64_t seed, int32_t spp, double* o, double* d, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,26 @@
+// bvh_build.h - host-side BVH (see bvh_build.cpp).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+namespace hrt {
+
+struct BvhNodeHost {        // layout identical to the device BvhNode (64 B)
+    double lo[3] = {0, 0, 0};
+    double hi[3] = {0, 0, 0};
+    int32_t first = 0;
+    int32_t count = 0;
+};
+static_assert(sizeof(BvhNodeHost) == 56, "node layout");
+
+struct BvhHost {
+    int32_t n_faces = 0;
+    std::vector<BvhNodeHost> nodes;
+    std::vector<double> tri;        // leaf order, 9 doubles per face
+    std::vector<int32_t> tri_id;    // leaf order -> global face id
+};
+
+BvhHost build_bvh(int64_t n_faces, const double* v0, const double* e1, const double* e2);
+void refit_bvh(BvhHost& b, const double* v0, const double* e1, const double* e2);
+
+}  // namespace hrt

@@ -1,0 +1,617 @@
+// hrt.cu - C ABI implementation (include/hrt.h): scene upload, BVH build,
+// weight packing, occupancy build, and the per-frame wavefront schedule.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hrt.h"
+#include "bvh_build.h"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(HRT_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+    } while (0)
+
+constexpr int64_t kMaxPaths = int64_t(1) << 22;   // paths per wavefront chunk
+constexpr int kThreads = 256;
+
+}  // namespace
+
+struct hrt_handle {
+    DevScene sc{};
+    std::vector<void*> allocs;
+    hrt::BvhHost bvh, blk;
+    BvhNode* d_nodes = nullptr;
+    double* d_tri = nullptr;
+    BvhNode* d_bnodes = nullptr;
+    double* d_btri = nullptr;
+    double* d_normal = nullptr;
+    int E = 0, F = 0;
+    int sm_count = 148;
+    // path-state arena
+    int64_t cap = 0;
+    void* arena = nullptr;
+    PathState ps{};
+    int32_t* trace = nullptr;
+    int64_t trace_cap = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    uint32_t* occ_dev = nullptr;
+    int64_t occ_words = 0;
+
+    template <class T>
+    int upload(const T* src, size_t n, T** dst) {
+        *dst = nullptr;
+        if (n == 0 || src == nullptr) return HRT_OK;
+        void* p = nullptr;
+        CK(cudaMalloc(&p, n * sizeof(T)));
+        allocs.push_back(p);
+        CK(cudaMemcpy(p, src, n * sizeof(T), cudaMemcpyHostToDevice));
+        *dst = static_cast<T*>(p);
+        return HRT_OK;
+    }
+    int alloc(size_t bytes, void** dst) {
+        CK(cudaMalloc(dst, bytes));
+        allocs.push_back(*dst);
+        return HRT_OK;
+    }
+    ~hrt_handle() {
+        for (void* p : allocs) cudaFree(p);
+        if (arena) cudaFree(arena);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+    }
+};
+
+namespace {
+
+int upload_bvh(hrt_handle* h, const hrt::BvhHost& b, DevBvh& out) {
+    out.n_faces = b.n_faces;
+    out.nodes = nullptr; out.tri = nullptr; out.tri_id = nullptr;
+    if (b.n_faces == 0) return HRT_OK;
+    static_assert(sizeof(BvhNode) == sizeof(hrt::BvhNodeHost), "node layout");
+    BvhNode* nodes;
+    double* tri;
+    int32_t* ids;
+    int rc;
+    if ((rc = h->upload(reinterpret_cast<const BvhNode*>(b.nodes.data()), b.nodes.size(), &nodes))) return rc;
+    if ((rc = h->upload(b.tri.data(), b.tri.size(), &tri))) return rc;
+    if ((rc = h->upload(b.tri_id.data(), b.tri_id.size(), &ids))) return rc;
+    out.nodes = nodes; out.tri = tri; out.tri_id = ids;
+    return HRT_OK;
+}
+
+// fp16 weights [K_in][N_out] row-major -> UMMA B image (N_pad x K_pad,
+// K-major core matrices), zero padded.
+void pack_layer(const uint16_t* w, int k_in, int n_out, int K, int N, uint8_t* dst) {
+    std::memset(dst, 0, (size_t)K * N * 2);
+    for (int n = 0; n < n_out; ++n)
+        for (int k = 0; k < k_in; ++k) {
+            const size_t off = (size_t)(n >> 3) * (K * 16) + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
+            std::memcpy(dst + off, &w[(size_t)k * n_out + n], 2);
+        }
+}
+
+int setup_field(hrt_handle* h, const hrt_field_desc& fd) {
+    DevField& f = h->sc.field;
+    f.kind = fd.kind;
+    f.identity = fd.identity;
+    for (int a = 0; a < 3; ++a) { f.lo[a] = fd.bbox_lo[a]; f.hi[a] = fd.bbox_hi[a]; }
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 4; ++c) f.inv[4 * r + c] = fd.field_from_world[4 * r + c];
+    int rc;
+    if (fd.kind == HRT_FIELD_DENSE) {
+        DenseGrid& g = f.dense;
+        const size_t n = (size_t)fd.res[0] * fd.res[1] * fd.res[2];
+        if (n == 0 || !fd.sigma || !fd.radiance) return fail(HRT_EINVAL, "dense field needs sigma/radiance");
+        for (int a = 0; a < 3; ++a) { g.res[a] = fd.res[a]; g.scale[a] = fd.scale[a]; }
+        double *s, *r;
+        if ((rc = h->upload(fd.sigma, n, &s))) return rc;
+        if ((rc = h->upload(fd.radiance, 3 * n, &r))) return rc;
+        g.sigma = s; g.rad = r;
+        g.sigma_const = fd.sigma_const; g.rad_const = fd.rad_const;
+        g.sigma0 = fd.sigma[0];
+        for (int c = 0; c < 3; ++c) g.rad0[c] = fd.radiance[c];
+    } else if (fd.kind == HRT_FIELD_NEURAL) {
+        NeuralField& nf = f.nf;
+        const int L = fd.n_levels, F = fd.n_features;
+        if (L < 1 || L > kMaxLevels || (F != 2 && F != 4)) return fail(HRT_EINVAL, "bad hash-grid shape");
+        const int E = L * F;
+        if (E != 16 && E != 32 && E != 64) return fail(HRT_EINVAL, "L*F must be 16, 32 or 64");
+        h->E = E; h->F = F;
+        nf.n_levels = L; nf.n_features = F; nf.enc_dim = E; nf.act = fd.act;
+        nf.tmask = (uint32_t)((1ull << fd.log2_table) - 1);
+        for (int a = 0; a < 3; ++a) nf.lo32[a] = (float)fd.bbox_lo[a];
+        for (int l = 0; l < L; ++l) {
+            NeuralLevel& lv = nf.lv[l];
+            for (int a = 0; a < 3; ++a) lv.scale[a] = fd.level_scale[3 * l + a];
+            lv.n = fd.level_n[l];
+            lv.r = (uint32_t)fd.level_n[l] + 1;
+            lv.dense = fd.level_dense[l];
+            lv.offset = fd.level_offset[l];
+        }
+        float* table;
+        if ((rc = h->upload(fd.table, (size_t)fd.n_entries * F, &table))) return rc;
+        nf.table = table;
+        const nerf::WOff W = nerf::woff(E);
+        std::vector<uint8_t> img(W.total);
+        pack_layer(fd.w_density1, E, 64, E, 64, img.data() + W.d1);
+        pack_layer(fd.w_density2, 64, 16, 64, 16, img.data() + W.d2);
+        pack_layer(fd.w_color1, 32, 64, 32, 64, img.data() + W.c1);
+        pack_layer(fd.w_color2, 64, 64, 64, 64, img.data() + W.c2);
+        pack_layer(fd.w_color3, 64, 3, 64, 16, img.data() + W.c3);
+        uint8_t* wp;
+        if ((rc = h->upload(img.data(), img.size(), &wp))) return rc;
+        nf.wpack = wp;
+        const int G = fd.occ_res;
+        nf.occ_res = G;
+        for (int a = 0; a < 3; ++a) {
+            nf.occ_scale[a] = fd.occ_scale[a];
+            nf.occ_cell[a] = (fd.bbox_hi[a] - fd.bbox_lo[a]) / G;
+        }
+        h->occ_words = ((int64_t)G * G * G + 31) / 32;
+        if (fd.occ_bits) {
+            if ((rc = h->upload(fd.occ_bits, (size_t)h->occ_words, &h->occ_dev))) return rc;
+        } else {
+            if ((rc = h->alloc((size_t)h->occ_words * 4, reinterpret_cast<void**>(&h->occ_dev)))) return rc;
+        }
+        nf.occ = h->occ_dev;
+    }
+    return HRT_OK;
+}
+
+template <int E, int F>
+int launch_field_eval(hrt_handle* h, const double* p, const double* d, int64_t n, float* sigma,
+                      float* rgb, int32_t* ev, int density_only, int use_occ, int field_frame,
+                      cudaStream_t st) {
+    constexpr uint32_t smem = 49152;   // caps residency at 4 CTAs/SM (TMEM: 4 x 128 cols)
+    static_assert(nerf::smem_layout(E).total <= smem, "smem");
+    CK(cudaFuncSetAttribute(kern::k_field_eval<E, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t tiles = (n + 127) / 128;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)h->sm_count * 4));
+    DevField f = h->sc.field;
+    if (field_frame) f.identity = 1;
+    kern::k_field_eval<E, F><<<grid, 128, smem, st>>>(f, p, d, n, sigma, rgb, ev, density_only, use_occ);
+    CK(cudaGetLastError());
+    return HRT_OK;
+}
+
+int field_eval(hrt_handle* h, const double* p, const double* d, int64_t n, float* sigma, float* rgb,
+               int32_t* ev, int density_only, int use_occ, int field_frame, cudaStream_t st) {
+    if (n == 0) return HRT_OK;
+    switch (h->E * 8 + h->F) {
+        case 16 * 8 + 2: return launch_field_eval<16, 2>(h, p, d, n, sigma, rgb, ev, density_only, use_occ, field_frame, st);
+        case 32 * 8 + 2: return launch_field_eval<32, 2>(h, p, d, n, sigma, rgb, ev, density_only, use_occ, field_frame, st);
+        case 64 * 8 + 4: return launch_field_eval<64, 4>(h, p, d, n, sigma, rgb, ev, density_only, use_occ, field_frame, st);
+        case 32 * 8 + 4: return launch_field_eval<32, 4>(h, p, d, n, sigma, rgb, ev, density_only, use_occ, field_frame, st);
+        case 64 * 8 + 2: return launch_field_eval<64, 2>(h, p, d, n, sigma, rgb, ev, density_only, use_occ, field_frame, st);
+        case 16 * 8 + 4: return launch_field_eval<16, 4>(h, p, d, n, sigma, rgb, ev, density_only, use_occ, field_frame, st);
+    }
+    return fail(HRT_EINVAL, "unsupported encoding width");
+}
+
+// Occupancy (P4): sigma at every cell centre (field frame) > threshold.
+int build_occupancy(hrt_handle* h, double thr) {
+    const NeuralField& nf = h->sc.field.nf;
+    const int G = nf.occ_res;
+    const int64_t n = (int64_t)G * G * G;
+    std::vector<double> pts(3 * (size_t)n);
+    const DevField& f = h->sc.field;
+    for (int z = 0; z < G; ++z)
+        for (int y = 0; y < G; ++y)
+            for (int x = 0; x < G; ++x) {
+                const int64_t c = x + (int64_t)G * (y + (int64_t)G * z);
+                const int ijk[3] = {x, y, z};
+                for (int a = 0; a < 3; ++a)
+                    pts[3 * c + a] = f.lo[a] + ((double)ijk[a] + 0.5) * ((f.hi[a] - f.lo[a]) / G);
+            }
+    double* dp = nullptr;
+    float* ds = nullptr;
+    CK(cudaMalloc(&dp, pts.size() * 8));
+    CK(cudaMalloc(&ds, (size_t)n * 4));
+    CK(cudaMemcpy(dp, pts.data(), pts.size() * 8, cudaMemcpyHostToDevice));
+    int rc = field_eval(h, dp, nullptr, n, ds, nullptr, nullptr, 1, 0, 1, 0);
+    if (rc == HRT_OK) {
+        const int64_t words = (n + 31) / 32;
+        kern::k_occ_bits<<<(unsigned)((words + 255) / 256), 256>>>(ds, n, thr, h->occ_dev);
+        if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+            rc = fail(HRT_ECUDA, "occupancy build failed");
+    }
+    cudaFree(dp);
+    cudaFree(ds);
+    return rc;
+}
+
+int ensure_state(hrt_handle* h, int64_t paths) {
+    if (paths <= h->cap) return HRT_OK;
+    if (h->arena) { cudaFree(h->arena); h->arena = nullptr; }
+    const int64_t n = paths;
+    const size_t dbl = (size_t)n * 8, i32 = (size_t)n * 4;
+    const size_t bytes = 14 * dbl + 6 * i32 + 64 * 4 + 256;
+    CK(cudaMalloc(&h->arena, bytes));
+    char* p = static_cast<char*>(h->arena);
+    auto take_d = [&]() { double* r = reinterpret_cast<double*>(p); p += dbl; return r; };
+    auto take_i = [&]() { int32_t* r = reinterpret_cast<int32_t*>(p); p += i32; return r; };
+    PathState& s = h->ps;
+    s.ox = take_d(); s.oy = take_d(); s.oz = take_d();
+    s.dx = take_d(); s.dy = take_d(); s.dz = take_d();
+    s.Lr = take_d(); s.Lg = take_d(); s.Lb = take_d();
+    s.Tr = take_d(); s.Tg = take_d(); s.Tb = take_d();
+    s.Tm = take_d(); s.t_hit = take_d();
+    s.neval = take_i(); s.face = take_i(); s.pix = take_i(); s.smp = take_i();
+    s.queue[0] = take_i(); s.queue[1] = take_i();
+    s.counters = reinterpret_cast<int32_t*>(p);
+    h->cap = n;
+    return HRT_OK;
+}
+
+unsigned grid_for(const hrt_handle* h, int64_t n) {
+    const int64_t g = (n + kThreads - 1) / kThreads;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)h->sm_count * 16));
+}
+
+template <int E, int F>
+int launch_march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream_t st) {
+    constexpr uint32_t smem = 49152;
+    static_assert(nerf::smem_layout(E).total <= smem, "smem");
+    CK(cudaFuncSetAttribute(kern::k_march_neural<E, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t want = (n_paths + 127) / 128;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)h->sm_count * 4));
+    kern::k_march_neural<E, F><<<grid, 128, smem, st>>>(a);
+    CK(cudaGetLastError());
+    return HRT_OK;
+}
+
+int march(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream_t st) {
+    if (h->sc.field.kind == HRT_FIELD_DENSE) {
+        kern::k_march_dense<<<grid_for(h, n_paths), kThreads, 0, st>>>(a);
+        CK(cudaGetLastError());
+        return HRT_OK;
+    }
+    switch (h->E * 8 + h->F) {
+        case 16 * 8 + 2: return launch_march_neural<16, 2>(h, a, n_paths, st);
+        case 32 * 8 + 2: return launch_march_neural<32, 2>(h, a, n_paths, st);
+        case 64 * 8 + 4: return launch_march_neural<64, 4>(h, a, n_paths, st);
+        case 32 * 8 + 4: return launch_march_neural<32, 4>(h, a, n_paths, st);
+        case 64 * 8 + 2: return launch_march_neural<64, 2>(h, a, n_paths, st);
+        case 16 * 8 + 4: return launch_march_neural<16, 4>(h, a, n_paths, st);
+    }
+    return fail(HRT_EINVAL, "unsupported encoding width");
+}
+
+// Bounce loop of one chunk (render.py:204-246, or the degenerate tracers
+// render.py:249-299 for mode surface / volume).
+int run_bounces(hrt_handle* h, kern::Args& a, int64_t paths, int mode, cudaStream_t st) {
+    const bool field = h->sc.field.kind != HRT_FIELD_NONE;
+    const unsigned g = grid_for(h, paths);
+    int rc;
+    if (mode == HRT_MODE_VOLUME) {
+        a.bounce = 1;
+        a.cur = 0;
+        a.volume = 1;
+        kern::k_reset_queue<<<1, 1, 0, st>>>(h->ps.counters, 1);
+        if (field && (rc = march(h, a, paths, st))) return rc;
+        return HRT_OK;
+    }
+    for (int b = 1; b <= h->sc.n_bounces; ++b) {
+        a.bounce = b;
+        a.cur = (b - 1) & 1;
+        kern::k_reset_queue<<<1, 1, 0, st>>>(h->ps.counters, a.cur ^ 1);
+        kern::k_intersect<<<g, kThreads, 0, st>>>(a);
+        CK(cudaGetLastError());
+        if (field && mode == HRT_MODE_HYBRID && (rc = march(h, a, paths, st))) return rc;
+        kern::k_shade<<<g, kThreads, 0, st>>>(a);
+        CK(cudaGetLastError());
+    }
+    return HRT_OK;
+}
+
+path::Camera to_cam(const hrt_camera& c) {
+    path::Camera k{};
+    std::memcpy(k.rot, c.rot, sizeof(k.rot));
+    std::memcpy(k.pos, c.pos, sizeof(k.pos));
+    k.tan_half = c.tan_half;
+    k.aspect = c.aspect;
+    k.width = c.width;
+    k.height = c.height;
+    return k;
+}
+
+int strat_of(int spp) {
+    const int k = (int)std::floor(std::sqrt((double)spp));
+    return (k * k == spp && k > 1) ? k : 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hrt_last_error(void) { return g_err.c_str(); }
+int hrt_version(void) { return 1; }
+
+int hrt_create(const hrt_scene_desc* d, hrt_handle** out) {
+    if (!d || !out) return fail(HRT_EINVAL, "null argument");
+    *out = nullptr;
+    hrt_handle* h = new hrt_handle();
+    auto bail = [&](int rc) { delete h; return rc; };
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaEventCreate(&h->ev0));
+    CK(cudaEventCreate(&h->ev1));
+    DevScene& sc = h->sc;
+    int rc;
+    h->bvh = hrt::build_bvh(d->n_faces, d->v0, d->e1, d->e2);
+    h->blk = hrt::build_bvh(d->n_blockers, d->bv0, d->be1, d->be2);
+    if ((rc = upload_bvh(h, h->bvh, sc.bvh))) return bail(rc);
+    if ((rc = upload_bvh(h, h->blk, sc.blockers))) return bail(rc);
+    double *normal, *emission;
+    int32_t* mesh_of;
+    if ((rc = h->upload(d->normal, 3 * (size_t)d->n_faces, &normal))) return bail(rc);
+    if ((rc = h->upload(d->emission, 3 * (size_t)d->n_faces, &emission))) return bail(rc);
+    if ((rc = h->upload(d->mesh_of, (size_t)d->n_faces, &mesh_of))) return bail(rc);
+    sc.normal = normal; sc.emission = emission; sc.mesh_of = mesh_of;
+    h->d_normal = normal;
+    std::vector<double> r0(std::max(1, d->n_materials));
+    for (int m = 0; m < d->n_materials; ++m) {
+        const double q = (d->mat_ior[m] - 1.0) / (d->mat_ior[m] + 1.0);
+        r0[m] = std::pow(q, 2.0);
+    }
+    int32_t* mk_;
+    double *mrgb, *mior, *mr0;
+    if ((rc = h->upload(d->mat_kind, (size_t)d->n_materials, &mk_))) return bail(rc);
+    if ((rc = h->upload(d->mat_rgb, 3 * (size_t)d->n_materials, &mrgb))) return bail(rc);
+    if ((rc = h->upload(d->mat_ior, (size_t)d->n_materials, &mior))) return bail(rc);
+    if ((rc = h->upload(r0.data(), (size_t)d->n_materials, &mr0))) return bail(rc);
+    sc.mat = {mk_, mrgb, mior, mr0};
+    sc.em.n = d->n_emitters;
+    double *et, *ec, *er;
+    if ((rc = h->upload(d->emitter_tris, 9 * (size_t)d->n_emitters, &et))) return bail(rc);
+    if ((rc = h->upload(d->emitter_cdf, (size_t)d->n_emitters, &ec))) return bail(rc);
+    if ((rc = h->upload(d->emitter_rsrc, (size_t)d->n_emitters, &er))) return bail(rc);
+    sc.em.tris = et; sc.em.cdf = ec; sc.em.r_src = er;
+    if ((rc = setup_field(h, d->field))) return bail(rc);
+    sc.n_bounces = d->n_bounces;
+    sc.threshold = d->threshold;
+    sc.march_step = d->march_step;
+    sc.spawn_eps = d->spawn_eps;
+    sc.sample_cap = d->sample_cap;
+    sc.early_t = d->early_t;
+    if (!(d->march_step > 0)) return bail(fail(HRT_EINVAL, "march step must be > 0"));
+    if (d->field.kind == HRT_FIELD_NEURAL && !d->field.occ_bits) {
+        if ((rc = build_occupancy(h, d->field.occ_threshold))) return bail(rc);
+    }
+    CK(cudaDeviceSynchronize());
+    *out = h;
+    return HRT_OK;
+}
+
+int hrt_destroy(hrt_handle* h) {
+    delete h;
+    return HRT_OK;
+}
+
+int hrt_set_trace(hrt_handle* h, int32_t* records, int64_t cap) {
+    if (!h) return fail(HRT_EINVAL, "null handle");
+    h->trace = records;
+    h->trace_cap = cap;
+    return HRT_OK;
+}
+
+int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed, int32_t mode,
+               const int32_t* pixels, int64_t n_pixels, double* out, hrt_stats* stats, void* stream) {
+    if (!h || !cam || !out) return fail(HRT_EINVAL, "null argument");
+    if (spp < 1) return fail(HRT_EINVAL, "spp must be >= 1");
+    if (mode < 0 || mode > 2) return fail(HRT_EINVAL, "bad mode");
+    if (cam->width < 1 || cam->height < 1) return fail(HRT_EINVAL, "bad resolution");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t total_pix = pixels ? n_pixels : (int64_t)cam->width * cam->height;
+    const int64_t chunk_pix = std::max<int64_t>(1, kMaxPaths / spp);
+    int rc;
+    if ((rc = ensure_state(h, std::min<int64_t>(total_pix, chunk_pix) * spp))) return rc;
+    CK(cudaMemsetAsync(h->ps.counters, 0, 64 * 4, st));
+    CK(cudaEventRecord(h->ev0, st));
+    for (int64_t p0 = 0; p0 < total_pix; p0 += chunk_pix) {
+        const int64_t np = std::min(chunk_pix, total_pix - p0);
+        const int64_t paths = np * spp;
+        kern::Args a{};
+        a.sc = h->sc;
+        a.ps = h->ps;
+        a.cam = to_cam(*cam);
+        a.pixels = pixels ? pixels + p0 : nullptr;
+        a.pixel_base = pixels ? 0 : p0;
+        a.n_slots = np;
+        a.spp = spp;
+        a.strat = strat_of(spp);
+        a.seed = seed;
+        a.out = out;
+        a.out_offset = p0;
+        a.trace = h->trace;
+        a.trace_cap = h->trace_cap;
+        kern::k_raygen<<<grid_for(h, paths), kThreads, 0, st>>>(a);
+        CK(cudaGetLastError());
+        if ((rc = run_bounces(h, a, paths, mode, st))) return rc;
+        kern::k_accumulate<<<grid_for(h, np), kThreads, 0, st>>>(a);
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(h->ev1, st));
+    h->trace = nullptr;
+    int32_t ctr[64];
+    CK(cudaMemcpyAsync(ctr, h->ps.counters, sizeof(ctr), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (stats) {
+        stats->paths = total_pix * spp;
+        stats->nerf_samples = ctr[C_SAMPLES];
+        stats->shadow_rays = ctr[C_SHADOW];
+        stats->bounce_rays = ctr[C_SEGMENTS];
+        stats->trace_records = ctr[C_COUNT - 1];
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+        stats->ms = ms;
+    }
+    if (ctr[C_NONFINITE] != 0) return fail(HRT_ENONFINITE, "non-finite or negative radiance in frame");
+    return HRT_OK;
+}
+
+int hrt_trace_paths(hrt_handle* h, const double* o, const double* d, const int64_t* pixel,
+                    const int64_t* sample, int64_t n, uint64_t seed, int32_t mode, double* L,
+                    void* stream) {
+    if (!h || (n > 0 && (!o || !d || !pixel || !sample || !L))) return fail(HRT_EINVAL, "null argument");
+    if (mode < 0 || mode > 2) return fail(HRT_EINVAL, "bad mode");
+    if (n > kMaxPaths) return fail(HRT_EINVAL, "too many paths for one call");
+    if (n == 0) return HRT_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int rc;
+    if ((rc = ensure_state(h, n))) return rc;
+    CK(cudaMemsetAsync(h->ps.counters, 0, 64 * 4, st));
+    kern::Args a{};
+    a.sc = h->sc;
+    a.ps = h->ps;
+    a.n_slots = n;
+    a.spp = 1;
+    a.seed = seed;
+    kern::k_load_rays<<<grid_for(h, n), kThreads, 0, st>>>(a, o, d, pixel, sample);
+    CK(cudaGetLastError());
+    if ((rc = run_bounces(h, a, n, mode, st))) return rc;
+    kern::k_gather_L<<<grid_for(h, n), kThreads, 0, st>>>(a, L);
+    CK(cudaGetLastError());
+    int32_t ctr[64];
+    CK(cudaMemcpyAsync(ctr, h->ps.counters, sizeof(ctr), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (ctr[C_NONFINITE] != 0) return fail(HRT_ENONFINITE, "NaN radiance in path batch");
+    return HRT_OK;
+}
+
+int hrt_render_host(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed, int32_t mode,
+                    const int32_t* pixels, int64_t n_pixels, double* out, hrt_stats* stats) {
+    if (!h || !cam || !out) return fail(HRT_EINVAL, "null argument");
+    const int64_t npx = pixels ? n_pixels : (int64_t)cam->width * cam->height;
+    int32_t* dpix = nullptr;
+    double* dout = nullptr;
+    CK(cudaMalloc(&dout, (size_t)std::max<int64_t>(npx, 1) * 3 * 8));
+    if (pixels) {
+        CK(cudaMalloc(&dpix, (size_t)std::max<int64_t>(npx, 1) * 4));
+        CK(cudaMemcpy(dpix, pixels, (size_t)npx * 4, cudaMemcpyHostToDevice));
+    }
+    int rc = hrt_render(h, cam, spp, seed, mode, dpix, npx, dout, stats, nullptr);
+    if (rc == HRT_OK || rc == HRT_ENONFINITE) {
+        if (cudaMemcpy(out, dout, (size_t)npx * 3 * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+            rc = fail(HRT_ECUDA, "copy of the frame failed");
+    }
+    cudaFree(dout);
+    if (dpix) cudaFree(dpix);
+    return rc;
+}
+
+int hrt_refit(hrt_handle* h, const double* v0, const double* e1, const double* e2, const double* normal,
+              const double* bv0, const double* be1, const double* be2) {
+    if (!h) return fail(HRT_EINVAL, "null handle");
+    if (h->bvh.n_faces) {
+        hrt::refit_bvh(h->bvh, v0, e1, e2);
+        CK(cudaMemcpy(const_cast<BvhNode*>(h->sc.bvh.nodes), h->bvh.nodes.data(),
+                      h->bvh.nodes.size() * sizeof(BvhNode), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(const_cast<double*>(h->sc.bvh.tri), h->bvh.tri.data(), h->bvh.tri.size() * 8,
+                      cudaMemcpyHostToDevice));
+        if (normal)
+            CK(cudaMemcpy(h->d_normal, normal, 3 * (size_t)h->bvh.n_faces * 8, cudaMemcpyHostToDevice));
+    }
+    if (h->blk.n_faces && bv0) {
+        hrt::refit_bvh(h->blk, bv0, be1, be2);
+        CK(cudaMemcpy(const_cast<BvhNode*>(h->sc.blockers.nodes), h->blk.nodes.data(),
+                      h->blk.nodes.size() * sizeof(BvhNode), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(const_cast<double*>(h->sc.blockers.tri), h->blk.tri.data(), h->blk.tri.size() * 8,
+                      cudaMemcpyHostToDevice));
+    }
+    return HRT_OK;
+}
+
+int hrt_field_sample(hrt_handle* h, const double* points, const double* dirs, int64_t n, float* sigma,
+                     float* rgb, int32_t* evaluated, int32_t use_occupancy, void* stream) {
+    if (!h || (n > 0 && (!points || !sigma))) return fail(HRT_EINVAL, "null argument");
+    if (h->sc.field.kind != HRT_FIELD_NEURAL) return fail(HRT_EINVAL, "scene has no neural field");
+    if (dirs && !rgb) return fail(HRT_EINVAL, "rgb output required with dirs");
+    return field_eval(h, points, dirs, n, sigma, rgb, evaluated, dirs ? 0 : 1, use_occupancy, 0,
+                      static_cast<cudaStream_t>(stream));
+}
+
+int hrt_field_encode(hrt_handle* h, const double* points, int64_t n, float* features, uint32_t* indices,
+                     void* stream) {
+    if (!h || (n > 0 && (!points || !features))) return fail(HRT_EINVAL, "null argument");
+    if (h->sc.field.kind != HRT_FIELD_NEURAL) return fail(HRT_EINVAL, "scene has no neural field");
+    if (n == 0) return HRT_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned g = grid_for(h, n);
+    const DevField& f = h->sc.field;
+    switch (h->E * 8 + h->F) {
+        case 16 * 8 + 2: kern::k_field_encode<16, 2><<<g, kThreads, 0, st>>>(f, points, n, features, indices); break;
+        case 32 * 8 + 2: kern::k_field_encode<32, 2><<<g, kThreads, 0, st>>>(f, points, n, features, indices); break;
+        case 64 * 8 + 4: kern::k_field_encode<64, 4><<<g, kThreads, 0, st>>>(f, points, n, features, indices); break;
+        case 32 * 8 + 4: kern::k_field_encode<32, 4><<<g, kThreads, 0, st>>>(f, points, n, features, indices); break;
+        case 64 * 8 + 2: kern::k_field_encode<64, 2><<<g, kThreads, 0, st>>>(f, points, n, features, indices); break;
+        case 16 * 8 + 4: kern::k_field_encode<16, 4><<<g, kThreads, 0, st>>>(f, points, n, features, indices); break;
+        default: return fail(HRT_EINVAL, "unsupported encoding width");
+    }
+    CK(cudaGetLastError());
+    return HRT_OK;
+}
+
+int hrt_occupancy(hrt_handle* h, uint32_t* host_words, int64_t n_words) {
+    if (!h || !host_words) return fail(HRT_EINVAL, "null argument");
+    if (h->sc.field.kind != HRT_FIELD_NEURAL) return fail(HRT_EINVAL, "scene has no neural field");
+    if (n_words < h->occ_words) return fail(HRT_EINVAL, "buffer too small");
+    CK(cudaMemcpy(host_words, h->occ_dev, (size_t)h->occ_words * 4, cudaMemcpyDeviceToHost));
+    return HRT_OK;
+}
+
+int hrt_intersect(hrt_handle* h, int32_t blocker, int32_t any, const double* o, const double* d,
+                  const double* t_min, const double* t_max, int64_t n, double* t, int64_t* face,
+                  uint8_t* hit, void* stream) {
+    if (!h || (n > 0 && (!o || !d))) return fail(HRT_EINVAL, "null argument");
+    if (any ? !hit : (!t || !face)) return fail(HRT_EINVAL, "missing output");
+    if (n == 0) return HRT_OK;
+    const DevBvh& b = blocker ? h->sc.blockers : h->sc.bvh;
+    kern::k_rays<<<grid_for(h, n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        b, o, d, t_min, t_max, n, any, t, face, hit);
+    CK(cudaGetLastError());
+    return HRT_OK;
+}
+
+int hrt_uniform(const int64_t* keys, int64_t n, double* out, void* stream) {
+    if (n > 0 && (!keys || !out)) return fail(HRT_EINVAL, "null argument");
+    if (n == 0) return HRT_OK;
+    const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    kern::k_uniform<<<g, 256, 0, static_cast<cudaStream_t>(stream)>>>(keys, n, out);
+    CK(cudaGetLastError());
+    return HRT_OK;
+}
+
+int hrt_primary_rays(const hrt_camera* cam, const int64_t* pixel, const int64_t* sample, int64_t n,
+                     uint64_t seed, int32_t spp, double* o, double* d, void* stream) {
+    if (!cam || (n > 0 && (!pixel || !sample || !o || !d))) return fail(HRT_EINVAL, "null argument");
+    if (spp < 1) return fail(HRT_EINVAL, "spp must be >= 1");
+    if (n == 0) return HRT_OK;
+    const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    kern::k_primary<<<g, 256, 0, static_cast<cudaStream_t>(stream)>>>(to_cam(*cam), pixel, sample, n, seed,
+                                                                      strat_of(spp), o, d);
+    CK(cudaGetLastError());
+    return HRT_OK;
+}
+
+}  // extern "C"

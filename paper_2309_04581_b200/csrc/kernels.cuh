@@ -1,0 +1,510 @@
+// kernels.cuh - the wavefront render pipeline (one chunk of camera paths):
+//   k_raygen -> per bounce { k_intersect -> k_march_* -> k_shade } -> k_accumulate
+// Path state is SoA in HBM; the alive set is a ping-pong index queue whose
+// length lives on the device, so a whole frame launches without host syncs.
+#pragma once
+#include <cooperative_groups.h>
+#include "bvh.cuh"
+#include "common.cuh"
+#include "field_neural.cuh"
+#include "path.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace kern {
+
+struct Args {
+    DevScene sc;
+    PathState ps;
+    path::Camera cam;
+    const int32_t* pixels;   // pixel id per slot (nullptr: slot + pixel_base)
+    int64_t pixel_base;
+    int64_t n_slots;         // pixels in this chunk
+    int32_t spp, strat;
+    uint64_t seed;
+    int32_t bounce;          // 1-based
+    int32_t cur;             // current queue (0/1)
+    int32_t volume;          // degenerate tracer B: no surfaces, t_hit = inf
+    double* out;             // (n_slots, 3) device output
+    int64_t out_offset;      // slot offset in `out`
+    int32_t* trace;          // optional (path, bounce, k, cell) records
+    int64_t trace_cap;
+};
+
+// Warp-aggregated reservation of `n` slots on a device counter.
+HRT_DEV int32_t reserve(int32_t* ctr) {
+    cg::coalesced_group g = cg::coalesced_threads();
+    int32_t base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(ctr, (int32_t)g.size());
+    base = g.shfl(base, 0);
+    return base + (int32_t)g.thread_rank();
+}
+
+__global__ void k_raygen(Args a) {
+    const int64_t n = a.n_slots * a.spp;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t slot = p / a.spp, smp = p % a.spp;
+        const int64_t pix = a.pixels ? a.pixels[slot] : a.pixel_base + slot;
+        d3 o, d;
+        path::primary_ray(a.cam, pix, smp, a.seed, a.strat, o, d);
+        PathState& s = a.ps;
+        s.ox[p] = o.x; s.oy[p] = o.y; s.oz[p] = o.z;
+        s.dx[p] = d.x; s.dy[p] = d.y; s.dz[p] = d.z;
+        s.Lr[p] = s.Lg[p] = s.Lb[p] = 0.0;
+        s.Tr[p] = s.Tg[p] = s.Tb[p] = 1.0;
+        s.Tm[p] = 1.0;
+        s.neval[p] = 0;
+        s.pix[p] = (int32_t)pix;
+        s.smp[p] = (int32_t)smp;
+        s.t_hit[p] = INFINITY;
+        s.face[p] = -1;
+        s.queue[0][p] = (int32_t)p;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.ps.counters[C_Q0] = (int32_t)n;
+        a.ps.counters[C_Q1] = 0;
+    }
+}
+
+// trace_path (render.py:302-312): caller-supplied rays instead of camera rays.
+__global__ void k_load_rays(Args a, const double* o, const double* d, const int64_t* pix,
+                            const int64_t* smp) {
+    const int64_t n = a.n_slots;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        PathState& s = a.ps;
+        s.ox[p] = o[3 * p]; s.oy[p] = o[3 * p + 1]; s.oz[p] = o[3 * p + 2];
+        s.dx[p] = d[3 * p]; s.dy[p] = d[3 * p + 1]; s.dz[p] = d[3 * p + 2];
+        s.Lr[p] = s.Lg[p] = s.Lb[p] = 0.0;
+        s.Tr[p] = s.Tg[p] = s.Tb[p] = 1.0;
+        s.Tm[p] = 1.0;
+        s.neval[p] = 0;
+        s.pix[p] = (int32_t)pix[p];
+        s.smp[p] = (int32_t)smp[p];
+        s.t_hit[p] = INFINITY;
+        s.face[p] = -1;
+        s.queue[0][p] = (int32_t)p;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.ps.counters[C_Q0] = (int32_t)n;
+        a.ps.counters[C_Q1] = 0;
+    }
+}
+
+// K2: nearest hit of every alive path, t in (0, inf] (render.py:217).
+__global__ void k_intersect(Args a) {
+    const int32_t n = a.ps.counters[a.cur];
+    const int32_t* q = a.ps.queue[a.cur];
+    PathState& s = a.ps;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&s.counters[C_SEGMENTS], n);
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const int32_t p = q[j];
+        double t = INFINITY;
+        int32_t f = -1;
+        if (!a.volume)
+            f = bvh::closest(a.sc.bvh, mk(s.ox[p], s.oy[p], s.oz[p]), mk(s.dx[p], s.dy[p], s.dz[p]),
+                             0.0, INFINITY, t);
+        s.t_hit[p] = t;
+        s.face[p] = f;
+    }
+}
+
+// --------------------------------------------------------------- march
+// Segment of path p: [max(t0, 0), min(t1, t_hit)] against the field box
+// (render.py:142-148), midpoint count n = ceil(seg/dt) (field.py:218-220).
+struct Segment {
+    double s0, delta;
+    int32_t n;
+};
+
+HRT_DEV bool segment(const DevScene& sc, d3 o, d3 d, double t_end, Segment& g) {
+    const DevField& f = sc.field;
+    double t0, t1;
+    slab(f.lo, f.hi, field_point(f, o), field_dir(f, d), t0, t1);
+    const double s0 = fmax(t0, 0.0), s1 = fmin(t1, t_end);
+    if (!(s1 > s0)) return false;
+    const double seg = fmax(s1 - s0, 0.0);
+    double n = ceil(seg / sc.march_step);
+    if (seg > 0.0) n = fmax(n, 1.0); else n = 0.0;
+    g.s0 = s0;
+    g.n = (int32_t)n;
+    g.delta = seg / n;
+    return g.n > 0;
+}
+
+HRT_DEV d3 sample_point(d3 o, d3 d, const Segment& g, int32_t k) {
+    const double t = g.s0 + ((double)k + 0.5) * g.delta;
+    return {o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
+}
+
+struct Acc {
+    double L[3], Ts[3], T;
+    int32_t neval;
+};
+
+HRT_DEV void load_acc(const PathState& s, int32_t p, Acc& c) {
+    c.L[0] = s.Lr[p]; c.L[1] = s.Lg[p]; c.L[2] = s.Lb[p];
+    c.Ts[0] = s.Tr[p]; c.Ts[1] = s.Tg[p]; c.Ts[2] = s.Tb[p];
+    c.T = s.Tm[p];
+    c.neval = s.neval[p];
+}
+HRT_DEV void store_acc(const PathState& s, int32_t p, const Acc& c) {
+    s.Lr[p] = c.L[0]; s.Lg[p] = c.L[1]; s.Lb[p] = c.L[2];
+    s.Tr[p] = c.Ts[0]; s.Tg[p] = c.Ts[1]; s.Tb[p] = c.Ts[2];
+    s.Tm[p] = c.T;
+    s.neval[p] = c.neval;
+}
+
+// field.py:244-255 for one evaluated midpoint sample.
+HRT_DEV void composite(const Args& a, Acc& c, double sigma, const double rgb[3], double delta,
+                       d3 p, int32_t pix, int32_t smp, int32_t k) {
+    const double al = 1.0 - exp(-sigma * delta);
+    double m = 1.0;
+    if (a.sc.em.n > 0 && al > 0.0 && fmax(fmax(rgb[0], rgb[1]), rgb[2]) > 0.0) {
+        m = path::shadow_mask(a.sc, p, a.seed, pix, smp, a.bounce, k);
+        atomicAdd(&a.ps.counters[C_SHADOW], 1);
+    }
+    const double am = al * m;
+    for (int ch = 0; ch < 3; ++ch) c.L[ch] = c.L[ch] + (c.Ts[ch] * am) * rgb[ch];
+    const double keep = 1.0 - al;
+    for (int ch = 0; ch < 3; ++ch) c.Ts[ch] = c.Ts[ch] * keep;
+    c.T = c.T * keep;
+}
+
+HRT_DEV bool halted(const DevScene& sc, const Acc& c) {
+    if (sc.early_t > 0.0 && fmax(fmax(c.Ts[0], c.Ts[1]), c.Ts[2]) < sc.early_t) return true;
+    if (sc.sample_cap > 0 && c.neval >= sc.sample_cap) return true;
+    return false;
+}
+
+// Reference field plugin (dense RadianceGrid): one thread marches one path
+// through every midpoint of its segment, as march_arrays does.
+__global__ void k_march_dense(Args a) {
+    const int32_t n = a.ps.counters[a.cur];
+    const int32_t* q = a.ps.queue[a.cur];
+    const PathState& s = a.ps;
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const int32_t p = q[j];
+        const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+        Segment g;
+        if (!segment(a.sc, o, d, s.t_hit[p], g)) continue;
+        Acc c;
+        load_acc(s, p, c);
+        const int32_t pix = s.pix[p], smp = s.smp[p];
+        int32_t evals = 0;
+        for (int32_t k = 0; k < g.n; ++k) {
+            if (halted(a.sc, c)) break;
+            const d3 x = sample_point(o, d, g, k);
+            double rgb[3];
+            const double sigma = path::dense_sample(a.sc.field, x, rgb);
+            c.neval += 1;
+            ++evals;
+            composite(a, c, sigma, rgb, g.delta, x, pix, smp, k);
+        }
+        store_acc(s, p, c);
+        atomicAdd(&a.ps.counters[C_SAMPLES], evals);
+    }
+}
+
+// Occupancy DDA step: from an empty (or outside) sample k, the first index
+// that might leave the current cell. The cell box is shrunk by 1e-4 of a cell
+// so float32 cell assignment of later samples cannot disagree; one sample of
+// slack covers rounding of t. Every candidate is re-tested by position, so
+// the evaluated set equals the oracle's per-sample test exactly.
+HRT_DEV int32_t dda_next(const NeuralField& nf, const DevField& f, d3 of, d3 df, const Segment& g,
+                         int32_t k, const int32_t cell[3]) {
+    double lo[3], hi[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        const double eps = 1e-4 * nf.occ_cell[ax];
+        lo[ax] = f.lo[ax] + (double)cell[ax] * nf.occ_cell[ax] + eps;
+        hi[ax] = f.lo[ax] + (double)(cell[ax] + 1) * nf.occ_cell[ax] - eps;
+    }
+    double t0, t1;
+    slab(lo, hi, of, df, t0, t1);
+    if (!(t1 > t0)) return k + 1;
+    const double kk = ceil((t1 - g.s0) / g.delta - 0.5) - 1.0;
+    if (!(kk > (double)(k + 1))) return k + 1;
+    return kk >= (double)g.n ? g.n : (int32_t)kk;
+}
+
+// The paper's NeRF march: persistent CTAs of 128 path slots. Each round
+// every slot advances its path to the next occupied midpoint (refilling from
+// the alive queue with a warp-aggregated cursor when a path's segment ends),
+// the CTA evaluates the 128 samples through encode + tcgen05 MLP, and each
+// slot composites its own sample in order.
+template <int E, int F>
+__global__ void __launch_bounds__(128, 4) k_march_neural(Args a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const NeuralField& nf = a.sc.field.nf;
+    const DevField& fld = a.sc.field;
+    nerf::Tile tile = nerf::tile_setup<E>(nf, smem);
+    const int32_t nq = a.ps.counters[a.cur];
+    const int32_t* queue = a.ps.queue[a.cur];
+    const PathState& s = a.ps;
+
+    int32_t p = -1, k = 0, pix = 0, smp = 0;
+    d3 o{}, d{}, of{}, df{};
+    Segment g{};
+    Acc c{};
+    bool exhausted = false;
+    int32_t local_samples = 0;
+
+    while (true) {
+        bool have = false;
+        d3 x{}, xf{};
+        while (!exhausted && !have) {
+            if (p < 0) {
+                const int32_t j = reserve(&a.ps.counters[C_FETCH]);
+                if (j >= nq) { exhausted = true; break; }
+                const int32_t cand = queue[j];
+                const d3 co = mk(s.ox[cand], s.oy[cand], s.oz[cand]);
+                const d3 cd = mk(s.dx[cand], s.dy[cand], s.dz[cand]);
+                if (!segment(a.sc, co, cd, s.t_hit[cand], g)) continue;
+                p = cand; o = co; d = cd; of = field_point(fld, o); df = field_dir(fld, d);
+                k = 0; pix = s.pix[p]; smp = s.smp[p];
+                load_acc(s, p, c);
+            }
+            if (k >= g.n || halted(a.sc, c)) { store_acc(s, p, c); p = -1; continue; }
+            x = sample_point(o, d, g, k);
+            xf = field_point(fld, x);
+            if (!inside_box(fld.lo, fld.hi, xf)) { ++k; continue; }
+            int32_t cell3[3];
+            const int32_t cell = nerf::occ_cell(nf, xf, cell3);
+            if (nerf::occ_test(nf, cell)) {
+                have = true;
+                if (a.trace) {
+                    const int64_t slot = atomicAdd(&a.ps.counters[C_COUNT - 1], 1);
+                    if (slot < a.trace_cap) {
+                        int4 rec = make_int4(p, a.bounce, k, cell);
+                        reinterpret_cast<int4*>(a.trace)[slot] = rec;
+                    }
+                }
+            } else {
+                k = dda_next(nf, fld, of, df, g, k, cell3);
+            }
+        }
+        if (!__syncthreads_or(have)) break;
+        nerf::encode_row<E, F>(nf, xf, have, tile.A, threadIdx.x);
+        const d3 dir = field_dir(fld, d);
+        float rgbf[3];
+        const float sigma = nerf::mlp<E>(tile, nf, make_float3((float)dir.x, (float)dir.y, (float)dir.z),
+                                         false, rgbf);
+        if (have) {
+            const double rgb[3] = {(double)rgbf[0], (double)rgbf[1], (double)rgbf[2]};
+            c.neval += 1;
+            ++local_samples;
+            composite(a, c, (double)sigma, rgb, g.delta, x, pix, smp, k);
+            ++k;
+        }
+    }
+    nerf::tile_teardown(tile);
+    atomicAdd(&a.ps.counters[C_SAMPLES], local_samples);
+}
+
+// K8: hit shading, BSDF sample, spawn, compaction (render.py:221-244).
+__global__ void k_shade(Args a) {
+    const int32_t n = a.ps.counters[a.cur];
+    const int32_t* q = a.ps.queue[a.cur];
+    int32_t* next = a.ps.queue[a.cur ^ 1];
+    int32_t* next_n = &a.ps.counters[a.cur ^ 1];
+    const PathState& s = a.ps;
+    const DevScene& sc = a.sc;
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const int32_t p = q[j];
+        const int32_t f = s.face[p];
+        if (f < 0) continue;
+        const double t = s.t_hit[p];
+        const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+        const d3 point = {o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
+        const d3 n_raw = mk(sc.normal[3 * f], sc.normal[3 * f + 1], sc.normal[3 * f + 2]);
+        const bool facing = dot(n_raw, d) < 0.0;
+        const d3 nrm = facing ? n_raw : neg(n_raw);
+        Acc c;
+        load_acc(s, p, c);
+        if (facing) {
+            c.L[0] = c.L[0] + c.Ts[0] * sc.emission[3 * f];
+            c.L[1] = c.L[1] + c.Ts[1] * sc.emission[3 * f + 1];
+            c.L[2] = c.L[2] + c.Ts[2] * sc.emission[3 * f + 2];
+        }
+        const int32_t mi = sc.mesh_of[f];
+        const int32_t kind = sc.mat.kind[mi];
+        const d3 wo = neg(d);
+        const int32_t pix = s.pix[p], smp = s.smp[p];
+        d3 nd;
+        if (kind == 0) {
+            const double u1 = rng::uniform(a.seed, pix, smp, a.bounce, rng::BSDF_U, 0);
+            const double u2 = rng::uniform(a.seed, pix, smp, a.bounce, rng::BSDF_V, 0);
+            nd = path::cosine_sample(nrm, u1, u2);
+        } else if (kind == 1) {
+            nd = path::reflect(wo, nrm);
+        } else {
+            const double u = rng::uniform(a.seed, pix, smp, a.bounce, rng::BSDF_LOBE, 0);
+            nd = path::dielectric_sample(wo, nrm, facing, sc.mat.ior[mi], sc.mat.r0[mi], u);
+        }
+        for (int ch = 0; ch < 3; ++ch) c.Ts[ch] = c.Ts[ch] * sc.mat.rgb[3 * mi + ch];
+        s.ox[p] = point.x + sc.spawn_eps * nd.x;
+        s.oy[p] = point.y + sc.spawn_eps * nd.y;
+        s.oz[p] = point.z + sc.spawn_eps * nd.z;
+        s.dx[p] = nd.x; s.dy[p] = nd.y; s.dz[p] = nd.z;
+        store_acc(s, p, c);
+        if (fmax(fmax(c.Ts[0], c.Ts[1]), c.Ts[2]) >= sc.threshold) next[reserve(next_n)] = p;
+    }
+}
+
+__global__ void k_gather_L(Args a, double* out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < a.n_slots;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        out[3 * p] = a.ps.Lr[p];
+        out[3 * p + 1] = a.ps.Lg[p];
+        out[3 * p + 2] = a.ps.Lb[p];
+        if (!(isfinite(a.ps.Lr[p]) && isfinite(a.ps.Lg[p]) && isfinite(a.ps.Lb[p])))
+            atomicAdd(&a.ps.counters[C_NONFINITE], 1);
+    }
+}
+
+__global__ void k_reset_queue(int32_t* counters, int32_t which) {
+    counters[which] = 0;
+    counters[C_FETCH] = 0;
+}
+
+// Per-pixel sum over its spp paths in sample order, then / spp (render.py:348-350).
+__global__ void k_accumulate(Args a) {
+    const PathState& s = a.ps;
+    for (int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; slot < a.n_slots;
+         slot += (int64_t)gridDim.x * blockDim.x) {
+        double acc[3] = {0.0, 0.0, 0.0};
+        for (int32_t k = 0; k < a.spp; ++k) {
+            const int64_t p = slot * a.spp + k;
+            acc[0] = acc[0] + s.Lr[p];
+            acc[1] = acc[1] + s.Lg[p];
+            acc[2] = acc[2] + s.Lb[p];
+        }
+        double* o = a.out + 3 * (a.out_offset + slot);
+        bool bad = false;
+        for (int ch = 0; ch < 3; ++ch) {
+            const double v = acc[ch] / (double)a.spp;
+            o[ch] = v;
+            bad |= !(isfinite(v) && v >= 0.0);
+        }
+        if (bad) atomicAdd(&a.ps.counters[C_NONFINITE], 1);
+    }
+}
+
+// ------------------------------------------------- field-seam kernels
+// sample_batch(p, d) of the neural field on arbitrary points, plus the
+// density-only variant that builds the occupancy bitfield.
+template <int E, int F>
+__global__ void __launch_bounds__(128, 4) k_field_eval(DevField fld, const double* __restrict__ pts,
+                                                       const double* __restrict__ dirs, int64_t n,
+                                                       float* sigma_out, float* rgb_out,
+                                                       int32_t* evaluated, int32_t density_only,
+                                                       int32_t use_occupancy) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const NeuralField& nf = fld.nf;
+    nerf::Tile tile = nerf::tile_setup<E>(nf, smem);
+    const int64_t tiles = (n + 127) / 128;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t i = t * 128 + threadIdx.x;
+        bool valid = i < n;
+        d3 pf{}, df = mk(0.0, 0.0, 1.0);
+        if (valid) {
+            pf = field_point(fld, mk(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]));
+            if (dirs) df = field_dir(fld, mk(dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]));
+        }
+        bool ev = valid && inside_box(fld.lo, fld.hi, pf);
+        if (ev && use_occupancy) {
+            int32_t c3[3];
+            ev = nerf::occ_test(nf, nerf::occ_cell(nf, pf, c3));
+        }
+        nerf::encode_row<E, F>(nf, pf, ev, tile.A, threadIdx.x);
+        float rgb[3] = {0.f, 0.f, 0.f};
+        float sg = nerf::mlp<E>(tile, nf, make_float3((float)df.x, (float)df.y, (float)df.z),
+                                density_only != 0, rgb);
+        if (valid) {
+            sigma_out[i] = ev ? sg : 0.0f;
+            if (!density_only) {
+                rgb_out[3 * i] = ev ? rgb[0] : 0.f;
+                rgb_out[3 * i + 1] = ev ? rgb[1] : 0.f;
+                rgb_out[3 * i + 2] = ev ? rgb[2] : 0.f;
+            }
+            if (evaluated) evaluated[i] = ev ? 1 : 0;
+        }
+    }
+    nerf::tile_teardown(tile);
+}
+
+template <int E, int F>
+__global__ void k_field_encode(DevField fld, const double* __restrict__ pts, int64_t n, float* feat,
+                               uint32_t* index) {
+    const NeuralField& nf = fld.nf;
+    constexpr int L = E / F;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const d3 pf = field_point(fld, mk(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]));
+        const float3 rel = nerf::rel_coord(nf, pf);
+        for (int l = 0; l < L; ++l) {
+            float v[4];
+            nerf::encode_level<F>(nf, nf.lv[l], rel, v);
+            for (int j = 0; j < F; ++j) feat[i * E + l * F + j] = v[j];
+            if (index) {
+                const nerf::LevelCoord lc = nerf::level_coord(nf.lv[l], rel);
+                for (int c = 0; c < 8; ++c)
+                    index[(i * L + l) * 8 + c] = nerf::corner_index(nf.lv[l], lc, c, nf.tmask);
+            }
+        }
+    }
+}
+
+// Occupancy bits from sigma at cell centres (P4): bit set iff sigma > thr.
+__global__ void k_occ_bits(const float* sigma, int64_t n_cells, double thr, uint32_t* bits) {
+    const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (w * 32 >= n_cells) return;
+    uint32_t word = 0;
+    for (int b = 0; b < 32; ++b) {
+        const int64_t c = w * 32 + b;
+        if (c < n_cells && (double)sigma[c] > thr) word |= 1u << b;
+    }
+    bits[w] = word;
+}
+
+// --------------------------------------------------- parity probes (K1/K2)
+__global__ void k_uniform(const int64_t* keys, int64_t n, double* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t* k = keys + 6 * i;
+        out[i] = rng::uniform((uint64_t)k[0], k[1], k[2], k[3], k[4], k[5]);
+    }
+}
+
+__global__ void k_primary(path::Camera cam, const int64_t* pix, const int64_t* smp, int64_t n,
+                          uint64_t seed, int32_t strat, double* o, double* d) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        d3 oo, dd;
+        path::primary_ray(cam, pix[i], smp[i], seed, strat, oo, dd);
+        o[3 * i] = oo.x; o[3 * i + 1] = oo.y; o[3 * i + 2] = oo.z;
+        d[3 * i] = dd.x; d[3 * i + 1] = dd.y; d[3 * i + 2] = dd.z;
+    }
+}
+
+__global__ void k_rays(DevBvh b, const double* o, const double* d, const double* tmin,
+                       const double* tmax, int64_t n, int32_t any, double* t_out, int64_t* f_out,
+                       uint8_t* hit_out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const d3 oo = mk(o[3 * i], o[3 * i + 1], o[3 * i + 2]);
+        const d3 dd = mk(d[3 * i], d[3 * i + 1], d[3 * i + 2]);
+        const double t0 = tmin ? tmin[i] : 0.0, t1 = tmax ? tmax[i] : INFINITY;
+        if (any) {
+            hit_out[i] = bvh::any_hit(b, oo, dd, t0, t1) ? 1 : 0;
+        } else {
+            double t;
+            const int32_t f = bvh::closest(b, oo, dd, t0, t1, t);
+            t_out[i] = t;
+            f_out[i] = f;
+        }
+    }
+}
+
+}  // namespace kern

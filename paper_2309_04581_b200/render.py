@@ -1,0 +1,249 @@
+"""Drop-in render entry points (reference `hybridrt/render.py:302-401`).
+
+`render(scene, camera=None, spp=None, seed=None, threads=1) -> HdrImage`
+keeps the reference signature, argument meaning and errors (ValueError for
+spp < 1, AssertionError for non-finite/negative radiance) and accepts either
+this package's `Scene` or a reference `hybridrt.scene.Scene`. The scene is
+packed and uploaded once per (scene, geometry version) into a native
+`hrt_handle`; every frame then runs entirely in the sm_100a kernels of
+libhrt.so (include/hrt.h). `threads` is accepted for API compatibility;
+GPU work has no host thread pool.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .images import HdrImage, encode_pfm, encode_ppm
+from .pack import pack_camera, pack_scene, stratify_k  # noqa: F401  (re-export)
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+class Renderer:
+    """One uploaded scene on the current CUDA device."""
+
+    def __init__(self, scene_or_pack):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2309_04581_b200 renders on CUDA (sm_100a) only; no CPU path")
+        self.lib = _lib.load()
+        self.pack = scene_or_pack if isinstance(scene_or_pack, dict) else pack_scene(scene_or_pack)
+        keep = _lib._Keep()
+        desc = _lib.scene_desc(self.pack, keep)
+        handle = ctypes.c_void_p()
+        _lib.check(self.lib.hrt_create(ctypes.byref(desc), ctypes.byref(handle)), "hrt_create")
+        self.handle = handle
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.last_stats = {}
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.hrt_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ frames
+    def render_pixels(self, camera, spp, seed, mode=_lib.MODE_HYBRID, pixels=None, out=None):
+        """(n, 3) float64 device tensor for `pixels` (int32 device tensor of
+        pixel ids, None = whole frame in raster order)."""
+        if spp < 1:
+            raise ValueError("spp must be >= 1")
+        cam = _lib.camera_desc(camera if isinstance(camera, dict) else pack_camera(camera))
+        n = cam.width * cam.height if pixels is None else int(pixels.numel())
+        if out is None:
+            out = torch.empty((n, 3), dtype=torch.float64, device=self.device)
+        stats = _lib.Stats()
+        rc = self.lib.hrt_render(self.handle, ctypes.byref(cam), int(spp), int(seed) & (2**64 - 1),
+                                 int(mode), _dptr(pixels), n, _dptr(out), ctypes.byref(stats),
+                                 _stream())
+        self.last_stats = stats.as_dict()
+        _lib.check(rc, "hrt_render")
+        return out
+
+    def render_host(self, camera, spp, seed, mode=_lib.MODE_HYBRID, pixels=None, out=None):
+        """Same through host buffers (numpy in/out, copies inside the call)."""
+        cam = _lib.camera_desc(camera if isinstance(camera, dict) else pack_camera(camera))
+        pix = None if pixels is None else np.ascontiguousarray(pixels, np.int32)
+        n = cam.width * cam.height if pix is None else len(pix)
+        if out is None:
+            out = np.empty((n, 3), np.float64)
+        stats = _lib.Stats()
+        rc = self.lib.hrt_render_host(self.handle, ctypes.byref(cam), int(spp),
+                                      int(seed) & (2**64 - 1), int(mode),
+                                      None if pix is None else pix.ctypes.data_as(ctypes.c_void_p),
+                                      n, out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(stats))
+        self.last_stats = stats.as_dict()
+        _lib.check(rc, "hrt_render_host")
+        return out
+
+    def trace(self, o, d, pixel, sample, seed, mode=_lib.MODE_HYBRID):
+        """L (n,3) of caller rays (device tensors)."""
+        n = o.shape[0]
+        L = torch.empty((n, 3), dtype=torch.float64, device=self.device)
+        rc = self.lib.hrt_trace_paths(self.handle, _dptr(o), _dptr(d), _dptr(pixel), _dptr(sample),
+                                      n, int(seed) & (2**64 - 1), int(mode), _dptr(L), _stream())
+        _lib.check(rc, "hrt_trace_paths")
+        return L
+
+    def refit(self, scene):
+        pk = pack_scene(scene)
+        if len(pk["v0"]) != len(self.pack["v0"]) or len(pk["bv0"]) != len(self.pack["bv0"]):
+            raise ValueError("refit needs the same topology; build a new Renderer")
+        arrs = [np.ascontiguousarray(pk[k], np.float64) for k in
+                ("v0", "e1", "e2", "normal", "bv0", "be1", "be2")]
+        ptrs = [a.ctypes.data_as(ctypes.c_void_p) if a.size else None for a in arrs]
+        _lib.check(self.lib.hrt_refit(self.handle, *ptrs), "hrt_refit")
+        self.pack = pk
+
+    # ------------------------------------------------------------ probes
+    def field_sample(self, points, dirs=None, use_occupancy=False):
+        n = points.shape[0]
+        sigma = torch.empty(n, dtype=torch.float32, device=self.device)
+        rgb = torch.empty((n, 3), dtype=torch.float32, device=self.device) if dirs is not None else None
+        ev = torch.empty(n, dtype=torch.int32, device=self.device)
+        rc = self.lib.hrt_field_sample(self.handle, _dptr(points), _dptr(dirs), n, _dptr(sigma),
+                                       _dptr(rgb), _dptr(ev), int(use_occupancy), _stream())
+        _lib.check(rc, "hrt_field_sample")
+        return sigma, rgb, ev
+
+    def field_encode(self, points, with_index=True):
+        fp = self.pack["field"]
+        n = points.shape[0]
+        feat = torch.empty((n, fp["enc_dim"]), dtype=torch.float32, device=self.device)
+        idx = (torch.empty((n, fp["n_levels"], 8), dtype=torch.int32, device=self.device)
+               if with_index else None)
+        rc = self.lib.hrt_field_encode(self.handle, _dptr(points), n, _dptr(feat), _dptr(idx),
+                                       _stream())
+        _lib.check(rc, "hrt_field_encode")
+        return feat, idx
+
+    def occupancy(self):
+        g = self.pack["field"]["occ_res"]
+        words = np.zeros((g ** 3 + 31) // 32, np.uint32)
+        _lib.check(self.lib.hrt_occupancy(self.handle, words.ctypes.data_as(ctypes.c_void_p),
+                                          len(words)), "hrt_occupancy")
+        return words
+
+    def intersect(self, o, d, t_min=None, t_max=None, blocker=False, any_hit=False):
+        n = o.shape[0]
+        if any_hit:
+            hit = torch.empty(n, dtype=torch.uint8, device=self.device)
+            rc = self.lib.hrt_intersect(self.handle, int(blocker), 1, _dptr(o), _dptr(d),
+                                        _dptr(t_min), _dptr(t_max), n, None, None, _dptr(hit),
+                                        _stream())
+            _lib.check(rc, "hrt_intersect")
+            return hit.bool()
+        t = torch.empty(n, dtype=torch.float64, device=self.device)
+        f = torch.empty(n, dtype=torch.int64, device=self.device)
+        rc = self.lib.hrt_intersect(self.handle, int(blocker), 0, _dptr(o), _dptr(d), _dptr(t_min),
+                                    _dptr(t_max), n, _dptr(t), _dptr(f), None, _stream())
+        _lib.check(rc, "hrt_intersect")
+        return t, f
+
+    def set_trace(self, records, cap):
+        _lib.check(self.lib.hrt_set_trace(self.handle, _dptr(records), int(cap)), "hrt_set_trace")
+
+
+def uniform_keys(keys):
+    """rng.uniform over an (n, 6) int64 device tensor of key tuples."""
+    lib = _lib.load()
+    out = torch.empty(keys.shape[0], dtype=torch.float64, device=keys.device)
+    _lib.check(lib.hrt_uniform(_dptr(keys), keys.shape[0], _dptr(out), _stream()), "hrt_uniform")
+    return out
+
+
+def primary_rays(camera, pixel, sample, seed, spp):
+    lib = _lib.load()
+    cam = _lib.camera_desc(camera if isinstance(camera, dict) else pack_camera(camera))
+    n = pixel.shape[0]
+    o = torch.empty((n, 3), dtype=torch.float64, device=pixel.device)
+    d = torch.empty((n, 3), dtype=torch.float64, device=pixel.device)
+    _lib.check(lib.hrt_primary_rays(ctypes.byref(cam), _dptr(pixel), _dptr(sample), n,
+                                    int(seed) & (2**64 - 1), int(spp), _dptr(o), _dptr(d),
+                                    _stream()), "hrt_primary_rays")
+    return o, d
+
+
+# ------------------------------------------------------------------ cache
+
+def _geometry_key(scene):
+    # own Scene: explicit version; reference Scene: rebuild_bvh swaps the Bvh
+    return getattr(scene, "version", None), id(getattr(scene, "bvh", None))
+
+
+def renderer_for(scene) -> Renderer:
+    cached = getattr(scene, "_hrt_renderer", None)
+    key = _geometry_key(scene)
+    dev = torch.cuda.current_device()
+    if cached is not None and cached[2] == dev:
+        r = cached[1]
+        if cached[0] != key:
+            r.refit(scene)
+            scene._hrt_renderer = (key, r, dev)
+        return r
+    r = Renderer(scene)
+    scene._hrt_renderer = (key, r, dev)
+    return r
+
+
+def _resolve(scene, camera, spp, seed):
+    camera = camera or scene.camera
+    spp = scene.render.spp if spp is None else int(spp)
+    seed = scene.render.seed if seed is None else int(seed)
+    if spp < 1:
+        raise ValueError("spp must be >= 1")
+    return camera, spp, seed
+
+
+def _frame(scene, camera, spp, seed, mode):
+    camera, spp, seed = _resolve(scene, camera, spp, seed)
+    r = renderer_for(scene)
+    out = r.render_pixels(camera, spp, seed, mode)
+    w, h = camera.resolution
+    return HdrImage(out.cpu().numpy().reshape(h, w, 3))
+
+
+def render(scene, camera=None, spp=None, seed=None, threads=1) -> HdrImage:
+    """Average spp hybrid paths per pixel into a linear HDR image (render.py:372-380)."""
+    return _frame(scene, camera, spp, seed, _lib.MODE_HYBRID)
+
+
+def render_surface_only(scene, camera=None, spp=None, seed=None, threads=1) -> HdrImage:
+    """Degeneracy reference A: no volume marching (render.py:383-388)."""
+    return _frame(scene, camera, spp, seed, _lib.MODE_SURFACE)
+
+
+def render_volume_only(scene, camera=None, spp=None, seed=None, threads=1) -> HdrImage:
+    """Degeneracy reference B: one full-field march per camera ray (render.py:391-396)."""
+    return _frame(scene, camera, spp, seed, _lib.MODE_VOLUME)
+
+
+def trace_path(ray, scene, path_rng) -> np.ndarray:
+    """Linear radiance of one camera path keyed (seed, pixel, sample) (render.py:302-312)."""
+    r = renderer_for(scene)
+    dev = r.device
+    o = torch.tensor(np.asarray(ray.origin, np.float64).reshape(1, 3), device=dev)
+    d = torch.tensor(np.asarray(ray.dir, np.float64).reshape(1, 3), device=dev)
+    pix = torch.tensor([int(path_rng.pixel)], dtype=torch.int64, device=dev)
+    smp = torch.tensor([int(path_rng.sample)], dtype=torch.int64, device=dev)
+    return r.trace(o, d, pix, smp, int(path_rng.seed)).cpu().numpy()[0]
+
+
+def finalize(img: HdrImage, hdr_output: bool) -> bytes:
+    """PFM bytes for HDR output, else tone-mapped 8-bit PPM (render.py:399-401)."""
+    return encode_pfm(img) if hdr_output else encode_ppm(img)

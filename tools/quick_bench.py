@@ -1,0 +1,26 @@
+"""Quick device timing of one config's frames (development aid; bench.py is
+the contract)."""
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2309_04581_b200 import configs  # noqa: E402
+from paper_2309_04581_b200.render import Renderer  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+t0 = time.time()
+scene = configs.BUILDERS[cfg]()
+r = Renderer(scene)
+print(f"cfg{cfg} setup {time.time() - t0:.2f}s", flush=True)
+for it in range(4):
+    torch.cuda.synchronize()
+    t = time.time()
+    out = r.render_pixels(scene.camera, scene.render.spp, 0)
+    torch.cuda.synchronize()
+    dt = time.time() - t
+    s = r.last_stats
+    print(f"iter {it}: wall {dt*1e3:.1f} ms dev {s['ms']:.1f} ms samples {s['nerf_samples']:,} "
+          f"({s['nerf_samples']/s['ms']*1e3/1e9:.3f} G/s) paths {s['paths']:,} "
+          f"Mrays/s {s['paths']/s['ms']*1e3/1e6:.2f} mean {out.mean().item():.4f}", flush=True)
