@@ -126,6 +126,9 @@ typedef struct {
     int64_t bounce_rays;          /* closest-hit queries */
     int64_t trace_records;
     float ms;                     /* device time of the call */
+    float march_ms;               /* summed device time of the march launches */
+    int32_t march_launches;
+    int64_t launches;             /* kernels this library launched */
 } hrt_stats;
 
 const char* hrt_last_error(void);

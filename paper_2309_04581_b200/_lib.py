@@ -72,7 +72,9 @@ class CameraDesc(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("paths", ctypes.c_int64), ("nerf_samples", ctypes.c_int64),
                 ("shadow_rays", ctypes.c_int64), ("bounce_rays", ctypes.c_int64),
-                ("trace_records", ctypes.c_int64), ("ms", ctypes.c_float)]
+                ("trace_records", ctypes.c_int64), ("ms", ctypes.c_float),
+                ("march_ms", ctypes.c_float), ("march_launches", ctypes.c_int32),
+                ("launches", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
