@@ -128,20 +128,6 @@ def ncu_traffic():
         return None
 
 
-# ------------------------------------------------------------ tiles -----
-
-def rank_pixels(w, h, rank, world, tile=TILE):
-    import numpy as np
-    tx, ty = math.ceil(w / tile), math.ceil(h / tile)
-    ids = []
-    for t in range(rank, tx * ty, world):
-        x0, y0 = (t % tx) * tile, (t // tx) * tile
-        ys, xs = np.meshgrid(np.arange(y0, min(y0 + tile, h)), np.arange(x0, min(x0 + tile, w)),
-                             indexing="ij")
-        ids.append((ys * w + xs).reshape(-1))
-    return np.concatenate(ids).astype(np.int32) if ids else np.zeros(0, np.int32)
-
-
 # --------------------------------------------------- CPU baseline (oracle) -
 
 _CPU_SCENE = None
@@ -255,7 +241,8 @@ def run_ours(args, rank, world, local):
     import torch.distributed as dist
 
     from paper_2309_04581_b200 import configs
-    from paper_2309_04581_b200.render import Renderer
+    from paper_2309_04581_b200.renderer import Renderer
+    from paper_2309_04581_b200.tiles import FrameGather, tile_pixels
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -266,17 +253,11 @@ def run_ours(args, rank, world, local):
     field = scene.field
     r = Renderer(scene)
     w, h = cams[0].resolution
-    pix_host = rank_pixels(w, h, rank, world)
+    pix_host = tile_pixels(w, h, rank, world)
     pix = torch.as_tensor(pix_host, device=dev)
     n_local = len(pix_host)
-    n_max = math.ceil(math.ceil(w / TILE) * math.ceil(h / TILE) / world) * TILE * TILE
-    out = torch.zeros((n_max, 3), dtype=torch.float64, device=dev)
-    frame = torch.zeros((w * h, 3), dtype=torch.float64, device=dev) if rank == 0 else None
-    gathered = torch.empty((world * n_max, 3), dtype=torch.float64, device=dev) if world > 1 else None
-    all_pix = None
-    if world > 1 and rank == 0:
-        lists = [rank_pixels(w, h, q, world) for q in range(world)]
-        all_pix = [torch.as_tensor(l.astype(np.int64), device=dev) for l in lists]
+    gather = FrameGather(w, h, rank, world, dev)
+    out = gather.local
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
@@ -288,13 +269,7 @@ def run_ours(args, rank, world, local):
             e0.record(stream)
         r.render_pixels(cam, 1, 0, pixels=pix, out=out[:n_local])
         st = dict(r.last_stats)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, out)
-            if rank == 0:
-                for q in range(world):
-                    frame.index_copy_(0, all_pix[q], gathered[q * n_max:q * n_max + len(all_pix[q])])
-        elif rank == 0:
-            frame.copy_(out[:n_local])
+        gather.gather()                    # frame assembled on rank 0 (NCCL all-gather)
         if timed:
             e1.record(stream)
             e1.synchronize()

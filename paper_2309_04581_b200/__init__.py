@@ -24,7 +24,7 @@ def __getattr__(name):
     # torch + libhrt.so are loaded on first use of the render path only, so
     # host-side scene construction works in a CPU-only process.
     if name in _RENDER_NAMES:
-        from . import render as _render
+        from . import renderer as _render
         return getattr(_render, name)
     raise AttributeError(name)
 

@@ -26,7 +26,7 @@ def uniform(*keys) -> np.ndarray:
     broadcasting of the six keys, evaluated on the current CUDA device."""
     import torch
 
-    from .render import uniform_keys
+    from .renderer import uniform_keys
     if len(keys) != 6:
         raise TypeError("uniform takes the six keys (seed, pixel, sample, bounce, purpose, lane)")
     cols = np.broadcast_arrays(*[np.asarray(k) for k in keys])

@@ -1,0 +1,60 @@
+"""Multi-GPU frame partition: 16x16 pixel tiles dealt
+round-robin to ranks, each rank renders its tiles with a replicated scene,
+and the frame is gathered to rank 0 over the process group (NCCL on B200s,
+gloo in the CPU tests). Every pixel's paths are keyed by the global pixel id
+(reference render.py:337), so any partition is bit-identical to one GPU."""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+TILE = 16
+
+
+def tile_pixels(w: int, h: int, rank: int, world: int, tile: int = TILE) -> np.ndarray:
+    """Global pixel ids (int32) of the tiles owned by `rank`, tile by tile,
+    rows inside a tile."""
+    tx, ty = math.ceil(w / tile), math.ceil(h / tile)
+    parts = []
+    for t in range(rank, tx * ty, world):
+        x0, y0 = (t % tx) * tile, (t // tx) * tile
+        ys, xs = np.meshgrid(np.arange(y0, min(y0 + tile, h)), np.arange(x0, min(x0 + tile, w)),
+                             indexing="ij")
+        parts.append((ys * w + xs).reshape(-1))
+    return np.concatenate(parts).astype(np.int32) if parts else np.zeros(0, np.int32)
+
+
+def max_pixels_per_rank(w: int, h: int, world: int, tile: int = TILE) -> int:
+    return max(len(tile_pixels(w, h, r, world, tile)) for r in range(world))
+
+
+class FrameGather:
+    """All-gather of per-rank (n_r, 3) radiance into a (w*h, 3) frame on
+    rank 0. Buffers are padded to the largest rank so one collective moves
+    the frame (torch.distributed: NCCL over NVLink on the B200 box)."""
+
+    def __init__(self, w, h, rank, world, device, dtype=None, group=None):
+        import torch
+        self.w, self.h, self.rank, self.world, self.group = w, h, rank, world, group
+        self.n_max = max_pixels_per_rank(w, h, world)
+        dtype = dtype or torch.float64
+        self.local = torch.zeros((self.n_max, 3), dtype=dtype, device=device)
+        self.parts = [torch.empty_like(self.local) for _ in range(world)]
+        self.index = [torch.as_tensor(tile_pixels(w, h, q, world).astype(np.int64), device=device)
+                      for q in range(world)]
+        self.frame = torch.zeros((w * h, 3), dtype=dtype, device=device) if rank == 0 else None
+
+    def gather(self):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.all_gather(self.parts, self.local, group=self.group)
+            parts = self.parts
+        else:
+            parts = [self.local]
+        if self.rank == 0:
+            for q in range(self.world):
+                n = len(self.index[q])
+                self.frame.index_copy_(0, self.index[q], parts[q][:n])
+        return self.frame

@@ -21,7 +21,7 @@ from paper_2309_04581_b200 import assets, configs
 from paper_2309_04581_b200.core import Transform
 from paper_2309_04581_b200.field import NeuralField, RadianceGrid
 from paper_2309_04581_b200.pack import pack_camera, pack_scene
-from paper_2309_04581_b200.render import Renderer, primary_rays, uniform_keys
+from paper_2309_04581_b200.renderer import Renderer, primary_rays, uniform_keys
 from paper_2309_04581_b200.scene import Camera, EmitterSet, make_scene
 from paper_2309_04581_b200.surface import Dielectric, Lambertian, Mirror, TriangleMesh
 

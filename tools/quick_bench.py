@@ -7,7 +7,7 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2309_04581_b200 import configs  # noqa: E402
-from paper_2309_04581_b200.render import Renderer  # noqa: E402
+from paper_2309_04581_b200.renderer import Renderer  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 t0 = time.time()
