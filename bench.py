@@ -194,7 +194,7 @@ def cpu_workers():
 
 def cpu_baseline_block(n_tiles=0):
     workers = cpu_workers()
-    n_tiles = n_tiles or max(8, 2 * workers)
+    n_tiles = n_tiles or max(16, 8 * workers)
     # warm the worker imports once with a tiny job so the timed sample is steady-state
     samples, paths, dt = cpu_sample(n_tiles, workers)
     return {"value": samples / dt, "unit": "samples/s", "cores": workers, "kind": "port",
