@@ -126,9 +126,11 @@ typedef struct {
     int64_t bounce_rays;          /* closest-hit queries */
     int64_t trace_records;
     float ms;                     /* device time of the call */
-    float march_ms;               /* summed device time of the march launches */
-    int32_t march_launches;
+    float field_ms;               /* summed device time of the field-engine launches */
+    int32_t field_launches;
     int64_t launches;             /* kernels this library launched */
+    int64_t evaluated;            /* field evaluations incl. speculative ones discarded by early-out */
+    int64_t rounds;               /* march rounds (generate -> field -> composite) */
 } hrt_stats;
 
 const char* hrt_last_error(void);

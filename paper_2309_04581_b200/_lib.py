@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhrt.so")
+LIB_PATH = os.environ.get("HRT_LIB", os.path.join(_HERE, "libhrt.so"))
 
 HRT_OK, HRT_EINVAL, HRT_ENONFINITE, HRT_ECUDA, HRT_ENOMEM = range(5)
 MODE_HYBRID, MODE_SURFACE, MODE_VOLUME = 0, 1, 2
@@ -73,8 +73,9 @@ class Stats(ctypes.Structure):
     _fields_ = [("paths", ctypes.c_int64), ("nerf_samples", ctypes.c_int64),
                 ("shadow_rays", ctypes.c_int64), ("bounce_rays", ctypes.c_int64),
                 ("trace_records", ctypes.c_int64), ("ms", ctypes.c_float),
-                ("march_ms", ctypes.c_float), ("march_launches", ctypes.c_int32),
-                ("launches", ctypes.c_int64)]
+                ("field_ms", ctypes.c_float), ("field_launches", ctypes.c_int32),
+                ("launches", ctypes.c_int64), ("evaluated", ctypes.c_int64),
+                ("rounds", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -155,7 +155,8 @@ struct PathState {
 };
 
 enum Counter { C_Q0 = 0, C_Q1 = 1, C_FETCH = 2, C_SAMPLES = 3, C_SHADOW = 4, C_SEGMENTS = 5,
-               C_NONFINITE = 6, C_COUNT = 8 };
+               C_NONFINITE = 6, C_TRACE = 7, C_MQ0 = 8, C_MQ1 = 9, C_NS = 10, C_EVALS = 11,
+               C_COUNT = 16 };
 
 HRT_DEV d3 field_point(const DevField& f, d3 p) {
     if (f.identity) return p;

@@ -49,6 +49,23 @@ HRT_DEV void store8(uint8_t* A, int m, int k0, int K, const float* v) {
     *reinterpret_cast<uint4*>(A + umma::layout_offset(m, k0, K)) = *reinterpret_cast<uint4*>(h);
 }
 
+// Store 4 consecutive features [k0, k0+4) (k0 % 4 == 0) of row m as fp16.
+HRT_DEV void store4(uint8_t* A, int m, int k0, int K, const float* v) {
+    __half2 h[2] = {__floats2half2_rn(v[0], v[1]), __floats2half2_rn(v[2], v[3])};
+    *reinterpret_cast<uint2*>(A + umma::layout_offset(m, k0, K)) = *reinterpret_cast<uint2*>(h);
+}
+
+// Store n (4, 8 or 16) consecutive features starting at k0.
+template <int N>
+HRT_DEV void store_n(uint8_t* A, int m, int k0, int K, const float* v) {
+    if constexpr (N == 4) {
+        store4(A, m, k0, K, v);
+    } else {
+#pragma unroll
+        for (int k = 0; k < N; k += 8) store8(A, m, k0 + k, K, v + k);
+    }
+}
+
 struct LevelCoord {
     int32_t i[3];
     float f[3];

@@ -1,0 +1,288 @@
+// field_ws.cuh - warp-specialized NeRF field engine (K5 + K6) for batches of
+// samples. The hash-grid encode and the tcgen05 MLP run in different warps,
+// and every MMA A operand lives in TMEM, so the L1 data pipe carries only
+// the table gathers (round-1 ncu: with A tiles in smem the pipe was 97 %
+// busy, ~45 % of it shared-memory operand traffic).
+//
+// CTA (persistent, one per SM, 512 TMEM columns):
+//   16 encode warps: warp w owns TMEM lanes 32*(w%4).. (= tile rows) and the
+//       level quarter q = w/4; per tile it gathers levels [qL/4, (q+1)L/4) of
+//       its 32 rows, packs fp16 pairs and tcgen05.st's them into the tile's
+//       stage columns, then arrives on full[s].
+//   1 MMA warp (one elected thread, no TMEM ld/st): per tile, waits full[s],
+//       issues D1 with A = stage s in TMEM (commit frees the stage and
+//       signals accf[g]), then D2, C1, C2, C3 with A = group g's activation
+//       columns, each after the epilogue's actr[g] arrival.
+//   2 epilogue groups x 4 warps (warp <-> lane quarter): group g = tile % 2
+//       turns each accumulator into the next layer's fp16 A operand
+//       (tcgen05.ld -> ReLU -> tcgen05.st) and writes (sigma, rgb).
+// TMEM columns: stages [0, 4*E/2); group g: accum [128+128g, +64),
+// activations [192+128g, +32). Weights (B operands) stay in smem.
+// Numerics equal field_neural.cuh / oracle/field.py (same encode, fp16
+// operands, fp32 accumulation).
+#pragma once
+#include <cuda_fp16.h>
+#include "common.cuh"
+#include "field_neural.cuh"
+#include "umma.cuh"
+
+namespace fws {
+
+#ifndef HRT_WS_GROUPS
+#define HRT_WS_GROUPS 2
+#endif
+#ifndef HRT_WS_STAGES
+#define HRT_WS_STAGES 4
+#endif
+constexpr int kEncWarps = 16;               // 4 level quarters x 4 lane quarters
+constexpr int kMlpGroups = HRT_WS_GROUPS;
+constexpr int kMlpWarps = 4 * kMlpGroups;
+constexpr int kThreads = 32 * (kEncWarps + kMlpWarps + 1);   // + MMA issuer warp
+constexpr int kStages = HRT_WS_STAGES;
+constexpr int kRows = 128;
+constexpr uint32_t kTmemCols = 512;
+
+// One sample of a batch: field-frame float32 position (exactly
+// float(field_point(p)), the encode input) and the owning path id (SH
+// direction lookup + composite bookkeeping).
+struct __align__(16) SampleIn {
+    float x, y, z;
+    int32_t path;
+};
+
+struct SmemPlan {
+    uint32_t w, bars, tslot, total;
+};
+__host__ __device__ constexpr SmemPlan plan(int E) {
+    return {0u, nerf::woff(E).total, nerf::woff(E).total + 256u, nerf::woff(E).total + 272u};
+}
+
+// barrier slots (8 B each): full[kStages] (encoders -> MMA), empty[kStages]
+// (MMA commit -> encoders), accf[g] (MMA commit -> epilogue g), actr[g]
+// (epilogue g -> MMA: activations written / accumulator consumed)
+__device__ __forceinline__ uint32_t bar_full(uint32_t base, int s) { return base + 8u * s; }
+__device__ __forceinline__ uint32_t bar_empty(uint32_t base, int s) { return base + 8u * (kStages + s); }
+__device__ __forceinline__ uint32_t bar_accf(uint32_t base, int g) { return base + 8u * (2 * kStages + g); }
+__device__ __forceinline__ uint32_t bar_actr(uint32_t base, int g) {
+    return base + 8u * (2 * kStages + kMlpGroups + g);
+}
+
+__device__ __forceinline__ void arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// D = A(TMEM, 128 x K) * B(smem, N x K)^T as K/16 UMMAs.
+__device__ __forceinline__ void issue_ts(uint32_t tmem_d, uint32_t tmem_a, int K, uint32_t b_addr,
+                                         int N) {
+    const uint32_t id = umma::idesc_f16(kRows, N);
+    for (int s = 0; s < K / 16; ++s)
+        umma::mma_f16_ts(tmem_d, tmem_a + 8u * s, umma::desc(b_addr + 256u * s, K * 16), id,
+                         s > 0 ? 1u : 0u);
+}
+
+// 64-wide layer epilogue: accum -> ReLU -> fp16 pairs -> activation columns.
+__device__ __forceinline__ void relu64_tmem(uint32_t accum, uint32_t act) {
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+        float v[16];
+        umma::ld16(accum + c0, v);
+        uint32_t h[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) h[i] = umma::pack_half2(fmaxf(v[2 * i], 0.f), fmaxf(v[2 * i + 1], 0.f));
+        umma::st<8>(act + c0 / 2, h);
+    }
+    umma::wait_st();
+}
+
+// Batch evaluation of n samples -> out[i] = (sigma, r, g, b).
+// dir32[path] is the field-frame unit direction; density_only skips the
+// colour head (rgb = 0).
+template <int E, int F>
+__global__ void __launch_bounds__(kThreads, 1)
+k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __restrict__ count,
+           int64_t n_fixed, const float4* __restrict__ dir32, float4* __restrict__ out,
+           int32_t density_only) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    constexpr SmemPlan P = plan(E);
+    constexpr nerf::WOff W = nerf::woff(E);
+    constexpr int L = E / F;
+    constexpr int NL = L / 4;                     // levels per encode thread
+    constexpr int NC = NL * F / 2;                // TMEM columns per encode thread
+    constexpr uint32_t kStageCols = E / 2;
+    const int warp = threadIdx.x >> 5;
+    const int64_t n = count ? (int64_t)*count : n_fixed;
+    const int64_t tiles = (n + kRows - 1) / kRows;
+
+    // ---- prologue: weights to smem, barriers, TMEM
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(nf.wpack);
+        uint4* dst = reinterpret_cast<uint4*>(smem + P.w);
+        for (uint32_t i = threadIdx.x; i < W.total / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    const uint32_t bars = umma::saddr(smem + P.bars);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + P.tslot);
+    if (warp == kEncWarps + kMlpWarps) umma::tmem_alloc(umma::saddr(tslot), kTmemCols);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            umma::mbar_init(bar_full(bars, s), kEncWarps * 32);
+            umma::mbar_init(bar_empty(bars, s), 1);
+        }
+        for (int g = 0; g < kMlpGroups; ++g) {
+            umma::mbar_init(bar_accf(bars, g), 1);
+            umma::mbar_init(bar_actr(bars, g), 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    umma::fence_async_smem();
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;   // this warp's TMEM lane quarter
+
+    if (warp < kEncWarps) {
+        // ================= encode warps =================
+        const int q = warp >> 2;                    // level quarter
+        const int r = (warp & 3) * 32 + (threadIdx.x & 31);   // row == TMEM lane
+        const float3 lo = make_float3(nf.lo32[0], nf.lo32[1], nf.lo32[2]);
+        int it = 0;
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+            const int s = it % kStages;
+            const uint32_t ph = (uint32_t)((it / kStages) & 1);
+            const int64_t i = t * kRows + r;
+            float v[NL * F];
+            if (i < n) {
+                const SampleIn si = in[i];
+                const float3 rel = make_float3(__fsub_rn(si.x, lo.x), __fsub_rn(si.y, lo.y),
+                                               __fsub_rn(si.z, lo.z));
+#pragma unroll
+                for (int j = 0; j < NL; ++j)
+                    nerf::encode_level<F>(nf, nf.lv[q * NL + j], rel, v + j * F);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NL * F; ++k) v[k] = 0.f;
+            }
+            uint32_t h[NC];
+#pragma unroll
+            for (int k = 0; k < NC; ++k) h[k] = umma::pack_half2(v[2 * k], v[2 * k + 1]);
+            // stage free? (the gathers above already overlapped the wait)
+            if (it >= kStages) umma::mbar_wait(bar_empty(bars, s), ph ^ 1u);
+            __syncwarp();
+            umma::fence_after();
+            umma::st<NC>(tmem + lane + (uint32_t)s * kStageCols + (uint32_t)(q * NC), h);
+            umma::wait_st();
+            umma::fence_before();
+            arrive(bar_full(bars, s));
+        }
+    } else if (warp < kEncWarps + kMlpWarps) {
+        // ================= epilogue groups =================
+        // Group g owns tiles j with j % kMlpGroups == g. Per layer: wait the
+        // accumulator (accf[g]), tcgen05.ld, activation, tcgen05.st the next
+        // A operand, then arrive actr[g] (also "accumulator consumed").
+        const int ew = warp - kEncWarps;
+        const int g = ew / 4;
+        const int m = (ew % 4) * 32 + (threadIdx.x & 31);   // row == TMEM lane
+        const uint32_t accum = tmem + 128u + 128u * g + lane;
+        const uint32_t act = accum + 64u;
+        const uint32_t accf = bar_accf(bars, g), actr = bar_actr(bars, g);
+        uint32_t aph = 0;
+        auto take = [&]() {
+            umma::mbar_wait(accf, aph);
+            aph ^= 1u;
+            __syncwarp();
+            umma::fence_after();
+        };
+        auto give = [&]() {
+            umma::fence_before();
+            arrive(actr);
+        };
+        int it = 0;
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+            if ((it % kMlpGroups) != g) continue;
+            const int64_t i = t * kRows + m;
+            float3 dir = make_float3(0.f, 0.f, 1.f);
+            if (i < n && !density_only) {
+                const float4 d4 = dir32[in[i].path];
+                dir = make_float3(d4.x, d4.y, d4.z);
+            }
+            take();                                         // D1 done
+            relu64_tmem(accum, act);
+            give();
+            take();                                         // D2 done
+            float o[16];
+            umma::ld16(accum, o);
+            const float sigma = expf(o[0]);
+            float rgb[3] = {0.f, 0.f, 0.f};
+            if (!density_only) {
+                float c[32];
+                nerf::sh16(dir.x, dir.y, dir.z, c);
+#pragma unroll
+                for (int k = 1; k < 16; ++k) c[15 + k] = o[k];
+                c[31] = 0.0f;
+                uint32_t hc[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) hc[k] = umma::pack_half2(c[2 * k], c[2 * k + 1]);
+                umma::st<16>(act, hc);
+                umma::wait_st();
+                give();
+                take();                                     // C1 done
+                relu64_tmem(accum, act);
+                give();
+                take();                                     // C2 done
+                relu64_tmem(accum, act);
+                give();
+                take();                                     // C3 done
+                umma::ld16(accum, o);
+                rgb[0] = nerf::out_act(o[0], nf.act);
+                rgb[1] = nerf::out_act(o[1], nf.act);
+                rgb[2] = nerf::out_act(o[2], nf.act);
+            }
+            give();                                         // accumulator free
+            if (i < n) out[i] = make_float4(sigma, rgb[0], rgb[1], rgb[2]);
+        }
+    } else if ((threadIdx.x & 31) == 0) {
+        // ================= MMA issuer (one thread) =================
+        // Walks tile pairs (one per group) layer by layer so one group's MMA
+        // overlaps the other group's epilogue.
+        const uint32_t wb = umma::saddr(smem + P.w);
+        const int nl = density_only ? 2 : 5;
+        const uint32_t boff[5] = {W.d1, W.d2, W.c1, W.c2, W.c3};
+        const int kdim[5] = {E, 64, 32, 64, 64};
+        const int ndim[5] = {64, 16, 64, 64, 16};
+        int64_t J = 0;
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) ++J;
+        uint32_t rph[kMlpGroups] = {};
+        bool fresh[kMlpGroups];
+        for (int g = 0; g < kMlpGroups; ++g) fresh[g] = true;
+        for (int64_t j0 = 0; j0 < J; j0 += kMlpGroups) {
+            for (int k = 0; k < nl; ++k) {
+                for (int g = 0; g < kMlpGroups && j0 + g < J; ++g) {
+                    const int64_t j = j0 + g;
+                    const uint32_t accum = tmem + 128u + 128u * g;
+                    const uint32_t actr = bar_actr(bars, g);
+                    uint32_t a_src;
+                    if (k == 0) {
+                        const int s = (int)(j % kStages);
+                        umma::mbar_wait(bar_full(bars, s), (uint32_t)((j / kStages) & 1));
+                        if (!fresh[g]) { umma::mbar_wait(actr, rph[g]); rph[g] ^= 1u; }
+                        fresh[g] = false;
+                        a_src = tmem + (uint32_t)s * kStageCols;
+                    } else {
+                        umma::mbar_wait(actr, rph[g]);
+                        rph[g] ^= 1u;
+                        a_src = accum + 64u;
+                    }
+                    umma::fence_after();
+                    issue_ts(accum, a_src, kdim[k], wb + boff[k], ndim[k]);
+                    if (k == 0) umma::commit(bar_empty(bars, (int)(j % kStages)));
+                    umma::commit(bar_accf(bars, g));
+                }
+            }
+        }
+    }
+    umma::fence_before();
+    __syncthreads();
+    if (warp == kEncWarps + kMlpWarps) umma::tmem_free(tmem, kTmemCols);
+}
+
+}  // namespace fws

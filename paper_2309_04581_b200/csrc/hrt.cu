@@ -30,9 +30,10 @@ int fail(int code, const std::string& msg) {
             return fail(HRT_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
     } while (0)
 
-constexpr int64_t kMaxPaths = int64_t(1) << 22;   // paths per wavefront chunk
+constexpr int64_t kMaxPaths = int64_t(1) << 20;   // paths per wavefront chunk
 constexpr int kThreads = 256;
-constexpr int kTimedLaunches = 64;
+constexpr int kTimedLaunches = 256;
+constexpr int64_t kBatchCap = int64_t(1) << 24;   // samples per march round
 
 }  // namespace
 
@@ -54,7 +55,11 @@ struct hrt_handle {
     int32_t* trace = nullptr;
     int64_t trace_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    cudaEvent_t mev[2 * 64] = {};
+    cudaEvent_t mev[2 * 256] = {};
+    kern::MarchState ms{};
+    int64_t batch_cap = 0;
+    int32_t* pinned = nullptr;
+    int64_t rounds = 0;
     int n_timed = 0;
     int64_t launches = 0;
     uint32_t* occ_dev = nullptr;
@@ -82,6 +87,7 @@ struct hrt_handle {
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         for (cudaEvent_t e : mev) if (e) cudaEventDestroy(e);
+        if (pinned) cudaFreeHost(pinned);
     }
 };
 
@@ -182,34 +188,79 @@ int setup_field(hrt_handle* h, const hrt_field_desc& fd) {
     return HRT_OK;
 }
 
+// ------------------------------------------------------------ field engine
+unsigned grid_for(const hrt_handle* h, int64_t n) {
+    const int64_t g = (n + kThreads - 1) / kThreads;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)h->sm_count * 16));
+}
+
 template <int E, int F>
-int launch_field_eval(hrt_handle* h, const double* p, const double* d, int64_t n, float* sigma,
-                      float* rgb, int32_t* ev, int density_only, int use_occ, int field_frame,
-                      cudaStream_t st) {
-    constexpr uint32_t smem = 49152;   // caps residency at 4 CTAs/SM (TMEM: 4 x 128 cols)
-    static_assert(nerf::smem_layout(E).total <= smem, "smem");
-    CK(cudaFuncSetAttribute(kern::k_field_eval<E, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int64_t tiles = (n + 127) / 128;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)h->sm_count * 4));
-    DevField f = h->sc.field;
-    if (field_frame) f.identity = 1;
-    kern::k_field_eval<E, F><<<grid, 128, smem, st>>>(f, p, d, n, sigma, rgb, ev, density_only, use_occ);
+int launch_ws(hrt_handle* h, const fws::SampleIn* in, const int32_t* count, int64_t n_fixed,
+              int64_t n_max, const float4* dir32, float4* out, int density_only, cudaStream_t st) {
+    constexpr uint32_t smem = fws::plan(E).total;
+    CK(cudaFuncSetAttribute(fws::k_field_ws<E, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t tiles = (n_max + fws::kRows - 1) / fws::kRows;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)h->sm_count));
+    fws::k_field_ws<E, F><<<grid, fws::kThreads, smem, st>>>(h->sc.field.nf, in, count, n_fixed, dir32,
+                                                             out, density_only);
     CK(cudaGetLastError());
     return HRT_OK;
 }
 
+// Evaluate a batch (count on the device, at most n_max) with the field engine;
+// bracketed by events so the dominant kernel's device time is measured live.
+int field_ws(hrt_handle* h, const fws::SampleIn* in, const int32_t* count, int64_t n_fixed,
+             int64_t n_max, const float4* dir32, float4* out, int density_only, cudaStream_t st) {
+    if (n_max <= 0) return HRT_OK;
+    const bool timed = h->n_timed < kTimedLaunches;
+    if (timed) CK(cudaEventRecord(h->mev[2 * h->n_timed], st));
+    int rc;
+    switch (h->E * 8 + h->F) {
+        case 16 * 8 + 2: rc = launch_ws<16, 2>(h, in, count, n_fixed, n_max, dir32, out, density_only, st); break;
+        case 32 * 8 + 2: rc = launch_ws<32, 2>(h, in, count, n_fixed, n_max, dir32, out, density_only, st); break;
+        case 64 * 8 + 4: rc = launch_ws<64, 4>(h, in, count, n_fixed, n_max, dir32, out, density_only, st); break;
+        case 32 * 8 + 4: rc = launch_ws<32, 4>(h, in, count, n_fixed, n_max, dir32, out, density_only, st); break;
+        case 64 * 8 + 2: rc = launch_ws<64, 2>(h, in, count, n_fixed, n_max, dir32, out, density_only, st); break;
+        case 16 * 8 + 4: rc = launch_ws<16, 4>(h, in, count, n_fixed, n_max, dir32, out, density_only, st); break;
+        default: return fail(HRT_EINVAL, "unsupported encoding width");
+    }
+    if (rc) return rc;
+    if (timed) {
+        CK(cudaEventRecord(h->mev[2 * h->n_timed + 1], st));
+        ++h->n_timed;
+    }
+    ++h->launches;
+    return HRT_OK;
+}
+
+// sample_batch(p[, d]) on arbitrary device points (probe API + occupancy build).
 int field_eval(hrt_handle* h, const double* p, const double* d, int64_t n, float* sigma, float* rgb,
                int32_t* ev, int density_only, int use_occ, int field_frame, cudaStream_t st) {
     if (n == 0) return HRT_OK;
-    switch (h->E * 8 + h->F) {
-        case 16 * 8 + 2: return launch_field_eval<16, 2>(h, p, d, n, sigma, rgb, ev, density_only, use_occ, field_frame, st);
-        case 32 * 8 + 2: return launch_field_eval<32, 2>(h, p, d, n, sigma, rgb, ev, density_only, use_occ, field_frame, st);
-        case 64 * 8 + 4: return launch_field_eval<64, 4>(h, p, d, n, sigma, rgb, ev, density_only, use_occ, field_frame, st);
-        case 32 * 8 + 4: return launch_field_eval<32, 4>(h, p, d, n, sigma, rgb, ev, density_only, use_occ, field_frame, st);
-        case 64 * 8 + 2: return launch_field_eval<64, 2>(h, p, d, n, sigma, rgb, ev, density_only, use_occ, field_frame, st);
-        case 16 * 8 + 4: return launch_field_eval<16, 4>(h, p, d, n, sigma, rgb, ev, density_only, use_occ, field_frame, st);
+    void *in = nullptr, *dir = nullptr, *res = nullptr, *evb = nullptr;
+    CK(cudaMallocAsync(&in, (size_t)n * sizeof(fws::SampleIn), st));
+    CK(cudaMallocAsync(&res, (size_t)n * sizeof(float4), st));
+    if (d) CK(cudaMallocAsync(&dir, (size_t)n * sizeof(float4), st));
+    if (!ev) CK(cudaMallocAsync(&evb, (size_t)n * 4, st));
+    int32_t* e = ev ? ev : static_cast<int32_t*>(evb);
+    const unsigned g = grid_for(h, n);
+    DevField f = h->sc.field;
+    kern::k_field_prep<<<g, kThreads, 0, st>>>(f, p, d, n, use_occ, field_frame,
+                                               static_cast<fws::SampleIn*>(in),
+                                               static_cast<float4*>(dir), e);
+    CK(cudaGetLastError());
+    int rc = field_ws(h, static_cast<fws::SampleIn*>(in), nullptr, n, n, static_cast<float4*>(dir),
+                      static_cast<float4*>(res), density_only, st);
+    if (rc == HRT_OK) {
+        kern::k_field_post<<<g, kThreads, 0, st>>>(static_cast<float4*>(res), e, n, sigma,
+                                                   density_only ? nullptr : rgb);
+        CK(cudaGetLastError());
     }
-    return fail(HRT_EINVAL, "unsupported encoding width");
+    cudaFreeAsync(in, st);
+    cudaFreeAsync(res, st);
+    if (dir) cudaFreeAsync(dir, st);
+    if (evb) cudaFreeAsync(evb, st);
+    return rc;
 }
 
 // Occupancy (P4): sigma at every cell centre (field frame) > threshold.
@@ -248,12 +299,14 @@ int ensure_state(hrt_handle* h, int64_t paths) {
     if (paths <= h->cap) return HRT_OK;
     if (h->arena) { cudaFree(h->arena); h->arena = nullptr; }
     const int64_t n = paths;
-    const size_t dbl = (size_t)n * 8, i32 = (size_t)n * 4;
-    const size_t bytes = 14 * dbl + 6 * i32 + 64 * 4 + 256;
+    const int64_t nb = std::min<int64_t>(n * kern::kRoundSamples, kBatchCap);
+    const size_t dbl = (size_t)n * 8, i32 = (size_t)n * 4, f4 = (size_t)n * 16;
+    const size_t bytes = 16 * dbl + 12 * i32 + f4 + (size_t)nb * (16 + 4 + 16) + 64 * 4 + 1024;
     CK(cudaMalloc(&h->arena, bytes));
     char* p = static_cast<char*>(h->arena);
-    auto take_d = [&]() { double* r = reinterpret_cast<double*>(p); p += dbl; return r; };
-    auto take_i = [&]() { int32_t* r = reinterpret_cast<int32_t*>(p); p += i32; return r; };
+    auto take = [&](size_t b) { char* r = p; p += (b + 255) & ~size_t(255); return r; };
+    auto take_d = [&]() { return reinterpret_cast<double*>(take(dbl)); };
+    auto take_i = [&]() { return reinterpret_cast<int32_t*>(take(i32)); };
     PathState& s = h->ps;
     s.ox = take_d(); s.oy = take_d(); s.oz = take_d();
     s.dx = take_d(); s.dy = take_d(); s.dz = take_d();
@@ -262,56 +315,67 @@ int ensure_state(hrt_handle* h, int64_t paths) {
     s.Tm = take_d(); s.t_hit = take_d();
     s.neval = take_i(); s.face = take_i(); s.pix = take_i(); s.smp = take_i();
     s.queue[0] = take_i(); s.queue[1] = take_i();
-    s.counters = reinterpret_cast<int32_t*>(p);
+    kern::MarchState& m = h->ms;
+    m.s0 = take_d(); m.delta = take_d();
+    m.n = take_i(); m.k = take_i(); m.base = take_i(); m.cnt = take_i();
+    m.mq[0] = take_i(); m.mq[1] = take_i();
+    m.dir32 = reinterpret_cast<float4*>(take(f4));
+    m.in = reinterpret_cast<fws::SampleIn*>(take((size_t)nb * 16));
+    m.sk = reinterpret_cast<int32_t*>(take((size_t)nb * 4));
+    m.out = reinterpret_cast<float4*>(take((size_t)nb * 16));
+    s.counters = reinterpret_cast<int32_t*>(take(64 * 4));
     h->cap = n;
+    h->batch_cap = nb;
     return HRT_OK;
 }
 
-unsigned grid_for(const hrt_handle* h, int64_t n) {
-    const int64_t g = (n + kThreads - 1) / kThreads;
-    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)h->sm_count * 16));
+int read_counter(hrt_handle* h, int idx, cudaStream_t st, int32_t* v) {
+    CK(cudaMemcpyAsync(h->pinned, h->ps.counters + idx, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *v = *h->pinned;
+    return HRT_OK;
 }
 
-template <int E, int F>
-int launch_march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream_t st) {
-    constexpr uint32_t smem = 49152;
-    static_assert(nerf::smem_layout(E).total <= smem, "smem");
-    CK(cudaFuncSetAttribute(kern::k_march_neural<E, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int64_t want = (n_paths + 127) / 128;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)h->sm_count * 4));
-    kern::k_march_neural<E, F><<<grid, 128, smem, st>>>(a);
+// NeRF march of every alive path of this bounce: k_seg, then rounds of
+// k_gen -> k_field_ws -> k_comp until no path has midpoints left.
+int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream_t st) {
+    const unsigned g = grid_for(h, n_paths);
+    kern::k_round_reset<<<1, 1, 0, st>>>(h->ps.counters, 0);
+    kern::k_seg<<<g, kThreads, 0, st>>>(a, h->ms);
     CK(cudaGetLastError());
+    h->launches += 2;
+    int32_t live = 0;
+    int rc;
+    if ((rc = read_counter(h, C_MQ0, st, &live))) return rc;
+    int mc = 0;
+    while (live > 0) {
+        const int32_t S = (int32_t)std::max<int64_t>(
+            1, std::min<int64_t>(kern::kRoundSamples, h->batch_cap / live));
+        const unsigned gl = grid_for(h, live);
+        kern::k_round_reset<<<1, 1, 0, st>>>(h->ps.counters, mc ^ 1);
+        kern::k_gen<<<gl, kThreads, 0, st>>>(a, h->ms, mc, S);
+        CK(cudaGetLastError());
+        if ((rc = field_ws(h, h->ms.in, h->ps.counters + C_NS, 0, (int64_t)live * S, h->ms.dir32,
+                           h->ms.out, 0, st)))
+            return rc;
+        kern::k_comp<<<gl, kThreads, 0, st>>>(a, h->ms, mc);
+        CK(cudaGetLastError());
+        h->launches += 3;
+        ++h->rounds;
+        if ((rc = read_counter(h, C_MQ0 + (mc ^ 1), st, &live))) return rc;
+        mc ^= 1;
+    }
     return HRT_OK;
 }
 
-int march_dispatch(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream_t st) {
+int march(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream_t st) {
     if (h->sc.field.kind == HRT_FIELD_DENSE) {
         kern::k_march_dense<<<grid_for(h, n_paths), kThreads, 0, st>>>(a);
         CK(cudaGetLastError());
+        ++h->launches;
         return HRT_OK;
     }
-    switch (h->E * 8 + h->F) {
-        case 16 * 8 + 2: return launch_march_neural<16, 2>(h, a, n_paths, st);
-        case 32 * 8 + 2: return launch_march_neural<32, 2>(h, a, n_paths, st);
-        case 64 * 8 + 4: return launch_march_neural<64, 4>(h, a, n_paths, st);
-        case 32 * 8 + 4: return launch_march_neural<32, 4>(h, a, n_paths, st);
-        case 64 * 8 + 2: return launch_march_neural<64, 2>(h, a, n_paths, st);
-        case 16 * 8 + 4: return launch_march_neural<16, 4>(h, a, n_paths, st);
-    }
-    return fail(HRT_EINVAL, "unsupported encoding width");
-}
-
-// March launch bracketed by CUDA events on the launching stream so the
-// dominant kernel's device time is measured live (hrt_stats.march_ms).
-int march(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream_t st) {
-    const bool timed = h->n_timed < kTimedLaunches;
-    if (timed) CK(cudaEventRecord(h->mev[2 * h->n_timed], st));
-    int rc = march_dispatch(h, a, n_paths, st);
-    if (rc) return rc;
-    if (timed) CK(cudaEventRecord(h->mev[2 * h->n_timed + 1], st));
-    if (timed) ++h->n_timed;
-    ++h->launches;
-    return HRT_OK;
+    return march_neural(h, a, n_paths, st);
 }
 
 // Bounce loop of one chunk (render.py:204-246, or the degenerate tracers
@@ -377,6 +441,13 @@ int hrt_create(const hrt_scene_desc* d, hrt_handle** out) {
     CK(cudaEventCreate(&h->ev0));
     CK(cudaEventCreate(&h->ev1));
     for (cudaEvent_t& e : h->mev) CK(cudaEventCreate(&e));
+    CK(cudaMallocHost(&h->pinned, 64));
+    {   // keep stream-ordered scratch (probe batches) resident in the pool
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t keep = ~0ull;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     DevScene& sc = h->sc;
     int rc;
     h->bvh = hrt::build_bvh(d->n_faces, d->v0, d->e1, d->e2);
@@ -450,6 +521,7 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
     CK(cudaMemsetAsync(h->ps.counters, 0, 64 * 4, st));
     h->n_timed = 0;
     h->launches = 0;
+    h->rounds = 0;
     CK(cudaEventRecord(h->ev0, st));
     for (int64_t p0 = 0; p0 < total_pix; p0 += chunk_pix) {
         const int64_t np = std::min(chunk_pix, total_pix - p0);
@@ -485,7 +557,9 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
         stats->nerf_samples = ctr[C_SAMPLES];
         stats->shadow_rays = ctr[C_SHADOW];
         stats->bounce_rays = ctr[C_SEGMENTS];
-        stats->trace_records = ctr[C_COUNT - 1];
+        stats->trace_records = ctr[C_TRACE];
+        stats->evaluated = ctr[C_EVALS];
+        stats->rounds = h->rounds;
         float ms = 0.f;
         cudaEventElapsedTime(&ms, h->ev0, h->ev1);
         stats->ms = ms;
@@ -495,8 +569,8 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
             cudaEventElapsedTime(&x, h->mev[2 * i], h->mev[2 * i + 1]);
             mms += x;
         }
-        stats->march_ms = mms;
-        stats->march_launches = h->n_timed;
+        stats->field_ms = mms;
+        stats->field_launches = h->n_timed;
         stats->launches = h->launches;
     }
     if (ctr[C_NONFINITE] != 0) return fail(HRT_ENONFINITE, "non-finite or negative radiance in frame");
@@ -648,3 +722,4 @@ int hrt_primary_rays(const hrt_camera* cam, const int64_t* pixel, const int64_t*
 }
 
 }  // extern "C"
+

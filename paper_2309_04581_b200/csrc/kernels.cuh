@@ -7,6 +7,7 @@
 #include "bvh.cuh"
 #include "common.cuh"
 #include "field_neural.cuh"
+#include "field_ws.cuh"
 #include "path.cuh"
 
 namespace cg = cooperative_groups;
@@ -228,78 +229,149 @@ HRT_DEV int32_t dda_next(const NeuralField& nf, const DevField& f, d3 of, d3 df,
     return kk >= (double)g.n ? g.n : (int32_t)kk;
 }
 
-// The paper's NeRF march: persistent CTAs of 128 path slots. Each round
-// every slot advances its path to the next occupied midpoint (refilling from
-// the alive queue with a warp-aggregated cursor when a path's segment ends),
-// the CTA evaluates the 128 samples through encode + tcgen05 MLP, and each
-// slot composites its own sample in order.
-template <int E, int F>
-__global__ void __launch_bounds__(128, 4) k_march_neural(Args a) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    const NeuralField& nf = a.sc.field.nf;
-    const DevField& fld = a.sc.field;
-    nerf::Tile tile = nerf::tile_setup<E>(nf, smem);
-    const int32_t nq = a.ps.counters[a.cur];
-    const int32_t* queue = a.ps.queue[a.cur];
+// ------------------------------------------------------ NeRF march rounds
+// The paper's NeRF march as a three-kernel round (SURVEY K4/K7 around the
+// field engine fws::k_field_ws):
+//   k_seg   once per bounce: segment [max(t0,0), min(t1,t_hit)], n, delta,
+//           field-frame fp32 direction; paths with a segment enter march queue 0
+//   k_gen   per round: each marching path walks (occupancy DDA) to its next
+//           <= kRoundSamples evaluable midpoints and appends them to the batch
+//   (k_field_ws evaluates the batch: encode + tcgen05 MLP)
+//   k_comp  per round: each path composites its samples in k order (fp64),
+//           with shadows, early-out and sample cap; unfinished paths go to
+//           the other march queue
+// The evaluated sample set and the compositing order equal the oracle's
+// per-sample march (oracle/tracer.py march), so parity is unchanged.
+constexpr int kRoundSamples = 32;
+
+struct MarchState {         // per path, valid while the path is marching
+    double* s0;
+    double* delta;
+    int32_t* n;
+    int32_t* k;             // next candidate midpoint
+    int32_t* base;          // batch slice of the current round
+    int32_t* cnt;
+    float4* dir32;          // field-frame direction (SH input)
+    int32_t* mq[2];         // march queues
+    fws::SampleIn* in;      // batch
+    int32_t* sk;            // midpoint index of each batch sample
+    float4* out;            // (sigma, rgb) of each batch sample
+};
+
+__global__ void k_seg(Args a, MarchState m) {
+    const int32_t n = a.ps.counters[a.cur];
+    const int32_t* q = a.ps.queue[a.cur];
     const PathState& s = a.ps;
-
-    int32_t p = -1, k = 0, pix = 0, smp = 0;
-    d3 o{}, d{}, of{}, df{};
-    Segment g{};
-    Acc c{};
-    bool exhausted = false;
-    int32_t local_samples = 0;
-
-    while (true) {
-        bool have = false;
-        d3 x{}, xf{};
-        while (!exhausted && !have) {
-            if (p < 0) {
-                const int32_t j = reserve(&a.ps.counters[C_FETCH]);
-                if (j >= nq) { exhausted = true; break; }
-                const int32_t cand = queue[j];
-                const d3 co = mk(s.ox[cand], s.oy[cand], s.oz[cand]);
-                const d3 cd = mk(s.dx[cand], s.dy[cand], s.dz[cand]);
-                if (!segment(a.sc, co, cd, s.t_hit[cand], g)) continue;
-                p = cand; o = co; d = cd; of = field_point(fld, o); df = field_dir(fld, d);
-                k = 0; pix = s.pix[p]; smp = s.smp[p];
-                load_acc(s, p, c);
-            }
-            if (k >= g.n || halted(a.sc, c)) { store_acc(s, p, c); p = -1; continue; }
-            x = sample_point(o, d, g, k);
-            xf = field_point(fld, x);
-            if (!inside_box(fld.lo, fld.hi, xf)) { ++k; continue; }
-            int32_t cell3[3];
-            const int32_t cell = nerf::occ_cell(nf, xf, cell3);
-            if (nerf::occ_test(nf, cell)) {
-                have = true;
-                if (a.trace) {
-                    const int64_t slot = atomicAdd(&a.ps.counters[C_COUNT - 1], 1);
-                    if (slot < a.trace_cap) {
-                        int4 rec = make_int4(p, a.bounce, k, cell);
-                        reinterpret_cast<int4*>(a.trace)[slot] = rec;
-                    }
-                }
-            } else {
-                k = dda_next(nf, fld, of, df, g, k, cell3);
-            }
-        }
-        if (!__syncthreads_or(have)) break;
-        nerf::encode_row<E, F>(nf, xf, have, tile.A, threadIdx.x);
-        const d3 dir = field_dir(fld, d);
-        float rgbf[3];
-        const float sigma = nerf::mlp<E>(tile, nf, make_float3((float)dir.x, (float)dir.y, (float)dir.z),
-                                         false, rgbf);
-        if (have) {
-            const double rgb[3] = {(double)rgbf[0], (double)rgbf[1], (double)rgbf[2]};
-            c.neval += 1;
-            ++local_samples;
-            composite(a, c, (double)sigma, rgb, g.delta, x, pix, smp, k);
-            ++k;
-        }
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const int32_t p = q[j];
+        const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+        Segment g;
+        if (!segment(a.sc, o, d, s.t_hit[p], g)) continue;
+        m.s0[p] = g.s0;
+        m.delta[p] = g.delta;
+        m.n[p] = g.n;
+        m.k[p] = 0;
+        const d3 df = field_dir(a.sc.field, d);
+        m.dir32[p] = make_float4((float)df.x, (float)df.y, (float)df.z, 0.f);
+        m.mq[0][reserve(&a.ps.counters[C_MQ0])] = p;
     }
-    nerf::tile_teardown(tile);
-    atomicAdd(&a.ps.counters[C_SAMPLES], local_samples);
+}
+
+__global__ void k_gen(Args a, MarchState m, int32_t mcur, int32_t S) {
+    const int32_t nq = a.ps.counters[C_MQ0 + mcur];
+    const int32_t* q = m.mq[mcur];
+    const PathState& s = a.ps;
+    const DevField& fld = a.sc.field;
+    const NeuralField& nf = fld.nf;
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += gridDim.x * blockDim.x) {
+        const int32_t p = q[j];
+        Acc c;
+        c.Ts[0] = s.Tr[p]; c.Ts[1] = s.Tg[p]; c.Ts[2] = s.Tb[p];
+        c.neval = s.neval[p];
+        int32_t budget = S;
+        if (a.sc.sample_cap > 0) budget = min(budget, a.sc.sample_cap - c.neval);
+        int32_t cnt = 0, k = m.k[p];
+        int32_t ks[kRoundSamples];
+        float3 ps[kRoundSamples];
+        if (!halted(a.sc, c)) {
+            const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+            Segment g{m.s0[p], m.delta[p], m.n[p]};
+            const d3 of = field_point(fld, o), df = field_dir(fld, d);
+            while (cnt < budget && k < g.n) {
+                const d3 xf = field_point(fld, sample_point(o, d, g, k));
+                if (!inside_box(fld.lo, fld.hi, xf)) { ++k; continue; }
+                int32_t cell3[3];
+                const int32_t cell = nerf::occ_cell(nf, xf, cell3);
+                if (nerf::occ_test(nf, cell)) {
+                    ks[cnt] = k;
+                    ps[cnt] = nerf::to_f32(xf);
+                    ++cnt;
+                    ++k;
+                } else {
+                    k = dda_next(nf, fld, of, df, g, k, cell3);
+                }
+            }
+        }
+        int32_t base = 0;
+        if (cnt > 0) base = atomicAdd(&a.ps.counters[C_NS], cnt);
+        for (int32_t i = 0; i < cnt; ++i) {
+            fws::SampleIn r;
+            r.x = ps[i].x; r.y = ps[i].y; r.z = ps[i].z; r.path = p;
+            m.in[base + i] = r;
+            m.sk[base + i] = ks[i];
+        }
+        m.base[p] = base;
+        m.cnt[p] = cnt;
+        m.k[p] = k;
+    }
+}
+
+__global__ void k_comp(Args a, MarchState m, int32_t mcur) {
+    const int32_t nq = a.ps.counters[C_MQ0 + mcur];
+    const int32_t* q = m.mq[mcur];
+    int32_t* next = m.mq[mcur ^ 1];
+    int32_t* next_n = &a.ps.counters[C_MQ0 + (mcur ^ 1)];
+    const PathState& s = a.ps;
+    const NeuralField& nf = a.sc.field.nf;
+    int32_t done = 0;
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += gridDim.x * blockDim.x) {
+        const int32_t p = q[j];
+        Acc c;
+        load_acc(s, p, c);
+        const int32_t base = m.base[p], cnt = m.cnt[p];
+        const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+        const Segment g{m.s0[p], m.delta[p], m.n[p]};
+        const int32_t pix = s.pix[p], smp = s.smp[p];
+        bool stop = false;
+        for (int32_t i = 0; i < cnt; ++i) {
+            if (halted(a.sc, c)) { stop = true; break; }
+            const int32_t k = m.sk[base + i];
+            const float4 f = m.out[base + i];
+            const double rgb[3] = {(double)f.y, (double)f.z, (double)f.w};
+            const d3 x = sample_point(o, d, g, k);
+            c.neval += 1;
+            ++done;
+            composite(a, c, (double)f.x, rgb, g.delta, x, pix, smp, k);
+            if (a.trace) {
+                const fws::SampleIn r = m.in[base + i];
+                int32_t c3[3];
+                const int32_t cell = nerf::occ_cell(nf, mk(r.x, r.y, r.z), c3);
+                const int64_t slot = atomicAdd(&a.ps.counters[C_TRACE], 1);
+                if (slot < a.trace_cap)
+                    reinterpret_cast<int4*>(a.trace)[slot] = make_int4(p, a.bounce, k, cell);
+            }
+        }
+        store_acc(s, p, c);
+        if (!stop && !halted(a.sc, c) && m.k[p] < g.n) next[reserve(next_n)] = p;
+    }
+    if (done) atomicAdd(&a.ps.counters[C_SAMPLES], done);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.ps.counters[C_EVALS], a.ps.counters[C_NS]);
+}
+
+// Start of a march round: empty the batch and the next march queue.
+__global__ void k_round_reset(int32_t* counters, int32_t next_mq) {
+    counters[C_NS] = 0;
+    counters[C_MQ0 + next_mq] = 0;
 }
 
 // K8: hit shading, BSDF sample, spawn, compaction (render.py:221-244).
@@ -392,46 +464,46 @@ __global__ void k_accumulate(Args a) {
 }
 
 // ------------------------------------------------- field-seam kernels
-// sample_batch(p, d) of the neural field on arbitrary points, plus the
-// density-only variant that builds the occupancy bitfield.
-template <int E, int F>
-__global__ void __launch_bounds__(128, 4) k_field_eval(DevField fld, const double* __restrict__ pts,
-                                                       const double* __restrict__ dirs, int64_t n,
-                                                       float* sigma_out, float* rgb_out,
-                                                       int32_t* evaluated, int32_t density_only,
-                                                       int32_t use_occupancy) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    const NeuralField& nf = fld.nf;
-    nerf::Tile tile = nerf::tile_setup<E>(nf, smem);
-    const int64_t tiles = (n + 127) / 128;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int64_t i = t * 128 + threadIdx.x;
-        bool valid = i < n;
-        d3 pf{}, df = mk(0.0, 0.0, 1.0);
-        if (valid) {
-            pf = field_point(fld, mk(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]));
-            if (dirs) df = field_dir(fld, mk(dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]));
-        }
-        bool ev = valid && inside_box(fld.lo, fld.hi, pf);
-        if (ev && use_occupancy) {
+// sample_batch(p, d) on arbitrary points through the field engine: prep
+// converts world fp64 points to the engine's field-frame fp32 batch, post
+// masks vacuum / empty-cell samples (evaluated = 0).
+__global__ void k_field_prep(DevField fld, const double* __restrict__ pts,
+                             const double* __restrict__ dirs, int64_t n, int32_t use_occupancy,
+                             int32_t field_frame, fws::SampleIn* in, float4* dir32, int32_t* ev) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const d3 pw = mk(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+        const d3 pf = field_frame ? pw : field_point(fld, pw);
+        bool e = inside_box(fld.lo, fld.hi, pf);
+        if (e && use_occupancy) {
             int32_t c3[3];
-            ev = nerf::occ_test(nf, nerf::occ_cell(nf, pf, c3));
+            e = nerf::occ_test(fld.nf, nerf::occ_cell(fld.nf, pf, c3));
         }
-        nerf::encode_row<E, F>(nf, pf, ev, tile.A, threadIdx.x);
-        float rgb[3] = {0.f, 0.f, 0.f};
-        float sg = nerf::mlp<E>(tile, nf, make_float3((float)df.x, (float)df.y, (float)df.z),
-                                density_only != 0, rgb);
-        if (valid) {
-            sigma_out[i] = ev ? sg : 0.0f;
-            if (!density_only) {
-                rgb_out[3 * i] = ev ? rgb[0] : 0.f;
-                rgb_out[3 * i + 1] = ev ? rgb[1] : 0.f;
-                rgb_out[3 * i + 2] = ev ? rgb[2] : 0.f;
-            }
-            if (evaluated) evaluated[i] = ev ? 1 : 0;
+        fws::SampleIn r;
+        const float3 p32 = nerf::to_f32(pf);
+        r.x = p32.x; r.y = p32.y; r.z = p32.z; r.path = (int32_t)i;
+        in[i] = r;
+        if (dirs) {
+            const d3 df = field_dir(fld, mk(dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]));
+            dir32[i] = make_float4((float)df.x, (float)df.y, (float)df.z, 0.f);
+        }
+        ev[i] = e ? 1 : 0;
+    }
+}
+
+__global__ void k_field_post(const float4* __restrict__ res, const int32_t* __restrict__ ev,
+                             int64_t n, float* sigma, float* rgb) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 r = res[i];
+        const bool e = ev[i] != 0;
+        sigma[i] = e ? r.x : 0.f;
+        if (rgb) {
+            rgb[3 * i] = e ? r.y : 0.f;
+            rgb[3 * i + 1] = e ? r.z : 0.f;
+            rgb[3 * i + 2] = e ? r.w : 0.f;
         }
     }
-    nerf::tile_teardown(tile);
 }
 
 template <int E, int F>

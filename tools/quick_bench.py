@@ -23,4 +23,6 @@ for it in range(4):
     s = r.last_stats
     print(f"iter {it}: wall {dt*1e3:.1f} ms dev {s['ms']:.1f} ms samples {s['nerf_samples']:,} "
           f"({s['nerf_samples']/s['ms']*1e3/1e9:.3f} G/s) paths {s['paths']:,} "
-          f"Mrays/s {s['paths']/s['ms']*1e3/1e6:.2f} mean {out.mean().item():.4f}", flush=True)
+          f"Mrays/s {s['paths']/s['ms']*1e3/1e6:.2f} mean {out.mean().item():.4f} | field {s['field_ms']:.1f} ms "
+          f"x{s['field_launches']} evaluated {s['evaluated']:,} rounds {s['rounds']} launches {s['launches']}",
+          flush=True)
