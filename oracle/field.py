@@ -16,7 +16,9 @@ unpinned, parity against this definition is what the GPU tests check):
   Corner c = (cx, cy, cz) = (c & 1, c >> 1 & 1, c >> 2) has weight
   (wx * wy) * wz with w = f or 1 - f, index dense  X + r*Y + r*r*Z (r = N_l+1)
   or hashed (X ^ Y*2654435761 ^ Z*805459861) & (T - 1) in uint32, and the
-  feature accumulates acc = acc + w * table[...] over c = 0..7 in float32.
+  feature accumulates acc = fma(w, table[...], acc) over c = 0..7 in float32
+  from +0 (correctly rounded fused multiply-add; oracle/native.c pins it with
+  glibc fmaf, the GPU uses fma.rn.f32x2).
 * MLP: float16 operands (features, hidden activations, weights), products
   exact, sums here in float64 (GPU: float32 tensor-core accumulation), ReLU
   then round-to-nearest float16 between layers; sigma = exp(z[0]);
@@ -55,6 +57,8 @@ def native():
         _LIB = ctypes.CDLL(out)
         _LIB.oracle_rotate_fma.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                            ctypes.c_void_p]
+        _LIB.oracle_corner_fma.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_void_p]
     return _LIB
 
 
@@ -64,6 +68,17 @@ def rotate_fma(v, rot):
     rot = np.ascontiguousarray(rot, np.float64)
     out = np.empty_like(v)
     native().oracle_rotate_fma(len(v), v.ctypes.data, rot.ctypes.data, out.ctypes.data)
+    return out
+
+
+def corner_fma(w, v):
+    """float32 (n, F): fma-accumulate 8 corner values v (n, 8, F) with
+    weights w (n, 8) in corner order (exact, via glibc fmaf)."""
+    w = np.ascontiguousarray(w, np.float32)
+    v = np.ascontiguousarray(v, np.float32)
+    n, F = v.shape[0], v.shape[2]
+    out = np.empty((n, F), np.float32)
+    native().oracle_corner_fma(n, F, w.ctypes.data, v.ctypes.data, out.ctypes.data)
     return out
 
 
@@ -147,11 +162,12 @@ def neural_encode(fp, pf, want_index=False):
         frac = x - cell.astype(np.float32)
         w_hi, w_lo = frac, one - frac
         r = nl + 1
-        acc = np.zeros((n, F), np.float32)
+        wts = np.empty((n, 8), np.float32)
+        vals = np.empty((n, 8, F), np.float32)
         for c in range(8):
             bits = (c & 1, (c >> 1) & 1, c >> 2)
             w = [w_hi[:, a] if bits[a] else w_lo[:, a] for a in range(3)]
-            wt = (w[0] * w[1]) * w[2]
+            wts[:, c] = (w[0] * w[1]) * w[2]
             cx, cy, cz = (cell[:, a] + bits[a] for a in range(3))
             if fp["level_dense"][lvl]:
                 idx = (cx + r * cy + r * r * cz).astype(np.uint64)
@@ -159,10 +175,10 @@ def neural_encode(fp, pf, want_index=False):
                 with np.errstate(over="ignore"):
                     idx = (cx.astype(np.uint64) ^ (cy.astype(np.uint64) * HASH_PY)
                            ^ (cz.astype(np.uint64) * HASH_PZ)) & mask
-            vals = table[int(fp["level_offset"][lvl]) + idx.astype(np.int64)]
-            acc = acc + wt[:, None] * vals
+            vals[:, c] = table[int(fp["level_offset"][lvl]) + idx.astype(np.int64)]
             if want_index:
                 index[:, lvl, c] = idx.astype(np.uint32)
+        acc = corner_fma(wts, vals)
         feat[:, lvl * F:(lvl + 1) * F] = acc
     return (feat, index) if want_index else feat
 

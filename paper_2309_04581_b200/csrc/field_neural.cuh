@@ -100,44 +100,92 @@ HRT_DEV float corner_weight(const LevelCoord& c, int corner) {
     return __fmul_rn(__fmul_rn(wx, wy), wz);
 }
 
-// Features of one level, F = 2 or 4, accumulated in corner order 0..7 with
-// separately rounded multiply and add (oracle/field.py neural_encode).
+// acc (two packed fp32) = fma(w, v, acc) per lane of the pair: one FFMA2.
+HRT_DEV void fma2(float2& acc, float w, float2 v) {
+    unsigned long long a = *reinterpret_cast<unsigned long long*>(&acc);
+    const unsigned long long b = *reinterpret_cast<const unsigned long long*>(&v);
+    unsigned long long ww;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(ww) : "f"(w));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(ww), "l"(b));
+    acc = *reinterpret_cast<float2*>(&a);
+}
+
+// Gather the 8 corner entries of one level and accumulate them in corner
+// order 0..7 as acc = fma(w, v, acc) from +0 (oracle/field.py neural_encode,
+// pinned by glibc fmaf in oracle/native.c). For F = 2, x-adjacent corners
+// whose entries form an aligned 16-byte pair (idx(c+1) == idx(c) ^ 1) are
+// fetched with one float4 load; level bases are 16-byte aligned (hrt.cu pads
+// level offsets).
 template <int F>
-HRT_DEV void encode_level(const NeuralField& nf, const NeuralLevel& lv, float3 rel, float* out) {
-    const LevelCoord c = level_coord(lv, rel);
-    uint32_t idx[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) idx[k] = corner_index(lv, c, k, nf.tmask);
-    float acc[F];
-#pragma unroll
-    for (int j = 0; j < F; ++j) acc[j] = 0.0f;
-    if (F == 2) {
-        const float2* base = reinterpret_cast<const float2*>(nf.table) + lv.offset;
+HRT_DEV void gather_accumulate(const float* __restrict__ lvl_base, const uint32_t idx[8],
+                               const float w[8], float* out) {
+    if constexpr (F == 2) {
+        const float2* base = reinterpret_cast<const float2*>(lvl_base);
         float2 v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = __ldg(base + idx[k]);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const float w = corner_weight(c, k);
-            acc[0] = __fadd_rn(acc[0], __fmul_rn(w, v[k].x));
-            acc[1] = __fadd_rn(acc[1], __fmul_rn(w, v[k].y));
+        for (int k = 0; k < 8; k += 2) {
+            if (idx[k + 1] == (idx[k] ^ 1u)) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(base + (idx[k] & ~1u)));
+                const bool hi = idx[k] & 1u;
+                v[k] = hi ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
+                v[k + 1] = hi ? make_float2(q.x, q.y) : make_float2(q.z, q.w);
+            } else {
+                v[k] = __ldg(base + idx[k]);
+                v[k + 1] = __ldg(base + idx[k + 1]);
+            }
         }
+        float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) fma2(acc, w[k], v[k]);
+        out[0] = acc.x;
+        out[1] = acc.y;
     } else {
-        const float4* base = reinterpret_cast<const float4*>(nf.table) + lv.offset;
+        const float4* base = reinterpret_cast<const float4*>(lvl_base);
         float4 v[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] = __ldg(base + idx[k]);
+        float2 a0 = make_float2(0.0f, 0.0f), a1 = make_float2(0.0f, 0.0f);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const float w = corner_weight(c, k);
-            acc[0] = __fadd_rn(acc[0], __fmul_rn(w, v[k].x));
-            acc[1] = __fadd_rn(acc[1], __fmul_rn(w, v[k].y));
-            acc[2] = __fadd_rn(acc[2], __fmul_rn(w, v[k].z));
-            acc[3] = __fadd_rn(acc[3], __fmul_rn(w, v[k].w));
+            fma2(a0, w[k], make_float2(v[k].x, v[k].y));
+            fma2(a1, w[k], make_float2(v[k].z, v[k].w));
         }
+        out[0] = a0.x; out[1] = a0.y; out[2] = a1.x; out[3] = a1.y;
     }
+}
+
+// One level of the encoding, F = 2 or 4 features. Dense and hashed levels
+// take separate (warp-uniform) branches; the per-axis hash products are
+// formed once ((Y+1)*P == Y*P + P in uint32) and the corner weights share
+// their x*y products, with the oracle's rounding order ((wx*wy)*wz).
+template <int F>
+HRT_DEV void encode_level(const NeuralField& nf, const NeuralLevel& lv, float3 rel, float* out) {
+    const LevelCoord c = level_coord(lv, rel);
+    const float gx = __fsub_rn(1.0f, c.f[0]), gy = __fsub_rn(1.0f, c.f[1]),
+                gz = __fsub_rn(1.0f, c.f[2]);
+    const float wxy[4] = {__fmul_rn(gx, gy), __fmul_rn(c.f[0], gy), __fmul_rn(gx, c.f[1]),
+                          __fmul_rn(c.f[0], c.f[1])};
+    float w[8];
 #pragma unroll
-    for (int j = 0; j < F; ++j) out[j] = acc[j];
+    for (int k = 0; k < 8; ++k) w[k] = __fmul_rn(wxy[k & 3], (k & 4) ? c.f[2] : gz);
+    const float* lvl_base = nf.table + (size_t)lv.offset * F;
+    const uint32_t X = (uint32_t)c.i[0], Y = (uint32_t)c.i[1], Z = (uint32_t)c.i[2];
+    uint32_t idx[8];
+    if (lv.dense) {
+        const uint32_t r = lv.r, rr = r * r;
+        const uint32_t b0 = X + r * Y + rr * Z;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            idx[k] = b0 + (uint32_t)(k & 1) + ((k & 2) ? r : 0u) + ((k & 4) ? rr : 0u);
+        gather_accumulate<F>(lvl_base, idx, w, out);
+    } else {
+        const uint32_t hy0 = Y * kHashY, hy1 = hy0 + kHashY;
+        const uint32_t hz0 = Z * kHashZ, hz1 = hz0 + kHashZ;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            idx[k] = ((X + (uint32_t)(k & 1)) ^ ((k & 2) ? hy1 : hy0) ^ ((k & 4) ? hz1 : hz0)) & nf.tmask;
+        gather_accumulate<F>(lvl_base, idx, w, out);
+    }
 }
 
 HRT_DEV float3 rel_coord(const NeuralField& nf, d3 pf) {

@@ -151,8 +151,8 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __res
             const uint32_t ph = (uint32_t)((it / kStages) & 1);
             const int64_t i = t * kRows + r;
             float v[NL * F];
-            if (i < n) {
-                const SampleIn si = in[i];
+            const SampleIn si = i < n ? in[i] : SampleIn{0.f, 0.f, 0.f, -1};
+            if (si.path >= 0) {
                 const float3 rel = make_float3(__fsub_rn(si.x, lo.x), __fsub_rn(si.y, lo.y),
                                                __fsub_rn(si.z, lo.z));
 #pragma unroll
@@ -201,8 +201,9 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __res
             if ((it % kMlpGroups) != g) continue;
             const int64_t i = t * kRows + m;
             float3 dir = make_float3(0.f, 0.f, 1.f);
-            if (i < n && !density_only) {
-                const float4 d4 = dir32[in[i].path];
+            const int32_t path = i < n ? in[i].path : -1;
+            if (path >= 0 && !density_only) {
+                const float4 d4 = dir32[path];
                 dir = make_float3(d4.x, d4.y, d4.z);
             }
             take();                                         // D1 done
@@ -238,7 +239,7 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __res
                 rgb[2] = nerf::out_act(o[2], nf.act);
             }
             give();                                         // accumulator free
-            if (i < n) out[i] = make_float4(sigma, rgb[0], rgb[1], rgb[2]);
+            if (path >= 0) out[i] = make_float4(sigma, rgb[0], rgb[1], rgb[2]);
         }
     } else if ((threadIdx.x & 31) == 0) {
         // ================= MMA issuer (one thread) =================

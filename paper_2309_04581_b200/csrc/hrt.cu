@@ -150,16 +150,29 @@ int setup_field(hrt_handle* h, const hrt_field_desc& fd) {
         nf.n_levels = L; nf.n_features = F; nf.enc_dim = E; nf.act = fd.act;
         nf.tmask = (uint32_t)((1ull << fd.log2_table) - 1);
         for (int a = 0; a < 3; ++a) nf.lo32[a] = (float)fd.bbox_lo[a];
+        // Device table: same entries, each level starting on an even entry
+        // (16-byte aligned pairs for the x-pair gathers in encode_level).
+        int64_t padded = 0;
+        std::vector<int64_t> dev_off(L);
+        for (int l = 0; l < L; ++l) {
+            const int64_t end = l + 1 < L ? fd.level_offset[l + 1] : fd.n_entries;
+            dev_off[l] = padded;
+            padded += ((end - fd.level_offset[l]) + 1) & ~int64_t(1);
+        }
+        std::vector<float> tab((size_t)padded * F, 0.0f);
         for (int l = 0; l < L; ++l) {
             NeuralLevel& lv = nf.lv[l];
             for (int a = 0; a < 3; ++a) lv.scale[a] = fd.level_scale[3 * l + a];
             lv.n = fd.level_n[l];
             lv.r = (uint32_t)fd.level_n[l] + 1;
             lv.dense = fd.level_dense[l];
-            lv.offset = fd.level_offset[l];
+            lv.offset = dev_off[l];
+            const int64_t end = l + 1 < L ? fd.level_offset[l + 1] : fd.n_entries;
+            std::memcpy(&tab[(size_t)dev_off[l] * F], fd.table + (size_t)fd.level_offset[l] * F,
+                        (size_t)(end - fd.level_offset[l]) * F * sizeof(float));
         }
         float* table;
-        if ((rc = h->upload(fd.table, (size_t)fd.n_entries * F, &table))) return rc;
+        if ((rc = h->upload(tab.data(), tab.size(), &table))) return rc;
         nf.table = table;
         const nerf::WOff W = nerf::woff(E);
         std::vector<uint8_t> img(W.total);
@@ -355,7 +368,7 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
         kern::k_round_reset<<<1, 1, 0, st>>>(h->ps.counters, mc ^ 1);
         kern::k_gen<<<gl, kThreads, 0, st>>>(a, h->ms, mc, S);
         CK(cudaGetLastError());
-        if ((rc = field_ws(h, h->ms.in, h->ps.counters + C_NS, 0, (int64_t)live * S, h->ms.dir32,
+        if ((rc = field_ws(h, h->ms.in, nullptr, (int64_t)live * S, (int64_t)live * S, h->ms.dir32,
                            h->ms.out, 0, st)))
             return rc;
         kern::k_comp<<<gl, kThreads, 0, st>>>(a, h->ms, mc);

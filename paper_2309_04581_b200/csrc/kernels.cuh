@@ -291,8 +291,9 @@ __global__ void k_gen(Args a, MarchState m, int32_t mcur, int32_t S) {
         int32_t budget = S;
         if (a.sc.sample_cap > 0) budget = min(budget, a.sc.sample_cap - c.neval);
         int32_t cnt = 0, k = m.k[p];
-        int32_t ks[kRoundSamples];
-        float3 ps[kRoundSamples];
+        // sample-major batch: the i-th sample of the path with queue rank j
+        // goes to row i * nq + j, so a warp's lanes are neighbouring paths
+        // (adjacent pixels) at the same step -> coherent table gathers
         if (!halted(a.sc, c)) {
             const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
             Segment g{m.s0[p], m.delta[p], m.n[p]};
@@ -303,8 +304,11 @@ __global__ void k_gen(Args a, MarchState m, int32_t mcur, int32_t S) {
                 int32_t cell3[3];
                 const int32_t cell = nerf::occ_cell(nf, xf, cell3);
                 if (nerf::occ_test(nf, cell)) {
-                    ks[cnt] = k;
-                    ps[cnt] = nerf::to_f32(xf);
+                    const float3 p32 = nerf::to_f32(xf);
+                    fws::SampleIn r;
+                    r.x = p32.x; r.y = p32.y; r.z = p32.z; r.path = p;
+                    m.in[(int64_t)cnt * nq + j] = r;
+                    m.sk[(int64_t)cnt * nq + j] = k;
                     ++cnt;
                     ++k;
                 } else {
@@ -312,15 +316,13 @@ __global__ void k_gen(Args a, MarchState m, int32_t mcur, int32_t S) {
                 }
             }
         }
-        int32_t base = 0;
-        if (cnt > 0) base = atomicAdd(&a.ps.counters[C_NS], cnt);
-        for (int32_t i = 0; i < cnt; ++i) {
+        for (int32_t i = cnt; i < S; ++i) {          // holes: skipped by the field engine
             fws::SampleIn r;
-            r.x = ps[i].x; r.y = ps[i].y; r.z = ps[i].z; r.path = p;
-            m.in[base + i] = r;
-            m.sk[base + i] = ks[i];
+            r.x = r.y = r.z = 0.f;
+            r.path = -1;
+            m.in[(int64_t)i * nq + j] = r;
         }
-        m.base[p] = base;
+        if (cnt) atomicAdd(&a.ps.counters[C_NS], cnt);
         m.cnt[p] = cnt;
         m.k[p] = k;
     }
@@ -338,22 +340,23 @@ __global__ void k_comp(Args a, MarchState m, int32_t mcur) {
         const int32_t p = q[j];
         Acc c;
         load_acc(s, p, c);
-        const int32_t base = m.base[p], cnt = m.cnt[p];
+        const int32_t cnt = m.cnt[p];
         const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
         const Segment g{m.s0[p], m.delta[p], m.n[p]};
         const int32_t pix = s.pix[p], smp = s.smp[p];
         bool stop = false;
         for (int32_t i = 0; i < cnt; ++i) {
             if (halted(a.sc, c)) { stop = true; break; }
-            const int32_t k = m.sk[base + i];
-            const float4 f = m.out[base + i];
+            const int64_t row = (int64_t)i * nq + j;
+            const int32_t k = m.sk[row];
+            const float4 f = m.out[row];
             const double rgb[3] = {(double)f.y, (double)f.z, (double)f.w};
             const d3 x = sample_point(o, d, g, k);
             c.neval += 1;
             ++done;
             composite(a, c, (double)f.x, rgb, g.delta, x, pix, smp, k);
             if (a.trace) {
-                const fws::SampleIn r = m.in[base + i];
+                const fws::SampleIn r = m.in[row];
                 int32_t c3[3];
                 const int32_t cell = nerf::occ_cell(nf, mk(r.x, r.y, r.z), c3);
                 const int64_t slot = atomicAdd(&a.ps.counters[C_TRACE], 1);
