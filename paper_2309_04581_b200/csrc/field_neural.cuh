@@ -100,6 +100,11 @@ HRT_DEV float corner_weight(const LevelCoord& c, int corner) {
     return __fmul_rn(__fmul_rn(wx, wy), wz);
 }
 
+#ifndef HRT_PAIR_GATHERS
+#define HRT_PAIR_GATHERS 0   // measured: coherent sample-major batches are issue-bound, pairing costs more than it saves
+#endif
+constexpr bool kPairGathers = HRT_PAIR_GATHERS;
+
 // acc (two packed fp32) = fma(w, v, acc) per lane of the pair: one FFMA2.
 HRT_DEV void fma2(float2& acc, float w, float2 v) {
     unsigned long long a = *reinterpret_cast<unsigned long long*>(&acc);
@@ -124,7 +129,7 @@ HRT_DEV void gather_accumulate(const float* __restrict__ lvl_base, const uint32_
         float2 v[8];
 #pragma unroll
         for (int k = 0; k < 8; k += 2) {
-            if (idx[k + 1] == (idx[k] ^ 1u)) {
+            if (kPairGathers && idx[k + 1] == (idx[k] ^ 1u)) {
                 const float4 q = __ldg(reinterpret_cast<const float4*>(base + (idx[k] & ~1u)));
                 const bool hi = idx[k] & 1u;
                 v[k] = hi ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
@@ -186,6 +191,48 @@ HRT_DEV void encode_level(const NeuralField& nf, const NeuralLevel& lv, float3 r
             idx[k] = ((X + (uint32_t)(k & 1)) ^ ((k & 2) ? hy1 : hy0) ^ ((k & 4) ? hz1 : hz0)) & nf.tmask;
         gather_accumulate<F>(lvl_base, idx, w, out);
     }
+}
+
+// Two-phase form of encode_level for F = 2, used to keep two levels of
+// gathers in flight per thread: issue() computes the corner indices and
+// starts the 8 loads, finish() forms the weights and accumulates (same
+// arithmetic, same order as encode_level).
+struct LevelLoads {
+    LevelCoord c;
+    float2 v[8];
+};
+
+HRT_DEV void level_issue(const NeuralField& nf, const NeuralLevel& lv, float3 rel, LevelLoads& g) {
+    g.c = level_coord(lv, rel);
+    const float2* base = reinterpret_cast<const float2*>(nf.table) + lv.offset;
+    const uint32_t X = (uint32_t)g.c.i[0], Y = (uint32_t)g.c.i[1], Z = (uint32_t)g.c.i[2];
+    if (lv.dense) {
+        const uint32_t r = lv.r, rr = r * r;
+        const uint32_t b0 = X + r * Y + rr * Z;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            g.v[k] = __ldg(base + (b0 + (uint32_t)(k & 1) + ((k & 2) ? r : 0u) + ((k & 4) ? rr : 0u)));
+    } else {
+        const uint32_t hy0 = Y * kHashY, hy1 = hy0 + kHashY;
+        const uint32_t hz0 = Z * kHashZ, hz1 = hz0 + kHashZ;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            g.v[k] = __ldg(base + (((X + (uint32_t)(k & 1)) ^ ((k & 2) ? hy1 : hy0) ^
+                                    ((k & 4) ? hz1 : hz0)) & nf.tmask));
+    }
+}
+
+HRT_DEV void level_finish(const LevelLoads& g, float* out) {
+    const LevelCoord& c = g.c;
+    const float gx = __fsub_rn(1.0f, c.f[0]), gy = __fsub_rn(1.0f, c.f[1]),
+                gz = __fsub_rn(1.0f, c.f[2]);
+    const float wxy[4] = {__fmul_rn(gx, gy), __fmul_rn(c.f[0], gy), __fmul_rn(gx, c.f[1]),
+                          __fmul_rn(c.f[0], c.f[1])};
+    float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) fma2(acc, __fmul_rn(wxy[k & 3], (k & 4) ? c.f[2] : gz), g.v[k]);
+    out[0] = acc.x;
+    out[1] = acc.y;
 }
 
 HRT_DEV float3 rel_coord(const NeuralField& nf, d3 pf) {

@@ -28,13 +28,29 @@
 
 namespace fws {
 
+// HRT_WS_PROFILE builds accumulate per-role cycle counts into ws_prof
+// (dev aid: [0] enc total, [1] enc wait-empty, [2] epi total, [3] epi
+// wait-accf, [4] mma total, [5] mma wait-full, [6] mma wait-actr).
+#ifdef HRT_WS_PROFILE
+__device__ unsigned long long ws_prof[8];
+#define WS_T0(v) const long long v = clock64()
+#define WS_ADD(i, t0) atomicAdd(&ws_prof[i], (unsigned long long)(clock64() - (t0)))
+#else
+#define WS_T0(v)
+#define WS_ADD(i, t0)
+#endif
+
 #ifndef HRT_WS_GROUPS
 #define HRT_WS_GROUPS 2
 #endif
 #ifndef HRT_WS_STAGES
 #define HRT_WS_STAGES 4
 #endif
+#ifndef HRT_WS_INFLIGHT
+#define HRT_WS_INFLIGHT 2
+#endif
 constexpr int kEncWarps = 16;               // 4 level quarters x 4 lane quarters
+constexpr int kInflight = HRT_WS_INFLIGHT;  // levels of gathers in flight per encode thread
 constexpr int kMlpGroups = HRT_WS_GROUPS;
 constexpr int kMlpWarps = 4 * kMlpGroups;
 constexpr int kThreads = 32 * (kEncWarps + kMlpWarps + 1);   // + MMA issuer warp
@@ -140,6 +156,7 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __res
     const uint32_t tmem = *tslot;
     const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;   // this warp's TMEM lane quarter
 
+    WS_T0(t_role);
     if (warp < kEncWarps) {
         // ================= encode warps =================
         const int q = warp >> 2;                    // level quarter
@@ -155,9 +172,22 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __res
             if (si.path >= 0) {
                 const float3 rel = make_float3(__fsub_rn(si.x, lo.x), __fsub_rn(si.y, lo.y),
                                                __fsub_rn(si.z, lo.z));
+                if constexpr (F == 2 && NL % kInflight == 0) {
+                    // kInflight levels of gathers in flight per thread
 #pragma unroll
-                for (int j = 0; j < NL; ++j)
-                    nerf::encode_level<F>(nf, nf.lv[q * NL + j], rel, v + j * F);
+                    for (int j = 0; j < NL; j += kInflight) {
+                        nerf::LevelLoads g[kInflight];
+#pragma unroll
+                        for (int u = 0; u < kInflight; ++u)
+                            nerf::level_issue(nf, nf.lv[q * NL + j + u], rel, g[u]);
+#pragma unroll
+                        for (int u = 0; u < kInflight; ++u) nerf::level_finish(g[u], v + (j + u) * F);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < NL; ++j)
+                        nerf::encode_level<F>(nf, nf.lv[q * NL + j], rel, v + j * F);
+                }
             } else {
 #pragma unroll
                 for (int k = 0; k < NL * F; ++k) v[k] = 0.f;
@@ -166,7 +196,9 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __res
 #pragma unroll
             for (int k = 0; k < NC; ++k) h[k] = umma::pack_half2(v[2 * k], v[2 * k + 1]);
             // stage free? (the gathers above already overlapped the wait)
+            WS_T0(tw);
             if (it >= kStages) umma::mbar_wait(bar_empty(bars, s), ph ^ 1u);
+            if ((threadIdx.x & 31) == 0) WS_ADD(1, tw);
             __syncwarp();
             umma::fence_after();
             umma::st<NC>(tmem + lane + (uint32_t)s * kStageCols + (uint32_t)(q * NC), h);
@@ -187,7 +219,9 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __res
         const uint32_t accf = bar_accf(bars, g), actr = bar_actr(bars, g);
         uint32_t aph = 0;
         auto take = [&]() {
+            WS_T0(tw);
             umma::mbar_wait(accf, aph);
+            if ((threadIdx.x & 31) == 0) WS_ADD(3, tw);
             aph ^= 1u;
             __syncwarp();
             umma::fence_after();
@@ -264,12 +298,18 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __res
                     uint32_t a_src;
                     if (k == 0) {
                         const int s = (int)(j % kStages);
+                        WS_T0(tf);
                         umma::mbar_wait(bar_full(bars, s), (uint32_t)((j / kStages) & 1));
+                        WS_ADD(5, tf);
+                        WS_T0(ta);
                         if (!fresh[g]) { umma::mbar_wait(actr, rph[g]); rph[g] ^= 1u; }
+                        WS_ADD(6, ta);
                         fresh[g] = false;
                         a_src = tmem + (uint32_t)s * kStageCols;
                     } else {
+                        WS_T0(ta);
                         umma::mbar_wait(actr, rph[g]);
+                        WS_ADD(6, ta);
                         rph[g] ^= 1u;
                         a_src = accum + 64u;
                     }
@@ -281,6 +321,10 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __res
             }
         }
     }
+#ifdef HRT_WS_PROFILE
+    if ((threadIdx.x & 31) == 0)
+        WS_ADD(warp < kEncWarps ? 0 : (warp < kEncWarps + kMlpWarps ? 2 : 4), t_role);
+#endif
     umma::fence_before();
     __syncthreads();
     if (warp == kEncWarps + kMlpWarps) umma::tmem_free(tmem, kTmemCols);

@@ -736,3 +736,14 @@ int hrt_primary_rays(const hrt_camera* cam, const int64_t* pixel, const int64_t*
 
 }  // extern "C"
 
+
+#ifdef HRT_WS_PROFILE
+// Dev builds only: read and reset the field-engine cycle counters.
+extern "C" int hrt_ws_profile(unsigned long long* out8) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out8, fws::ws_prof, 8 * sizeof(unsigned long long));
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(fws::ws_prof, z, sizeof(z));
+    return 0;
+}
+#endif
