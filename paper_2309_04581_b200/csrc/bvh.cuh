@@ -141,4 +141,68 @@ HRT_DEV bool any_hit(const DevBvh& b, d3 o, d3 d, double t_min, double t_max) {
     return false;
 }
 
+// ------------------------------------------------------------ GPU refit (K11)
+// Moving meshes keep their topology; the tree is refit bottom-up: each leaf
+// rebuilds its padded box from its (new) triangles, then climbs; at every
+// inner node the second child to arrive (arrival counter) forms the union.
+// Boxes use the host builder's padding rule (bvh_build.cpp face_box), so
+// hits stay exactly those of brute force.
+HRT_DEV void face_box_pad(const double* t9, double lo[3], double hi[3]) {
+    double ext = 0.0, mag = 1.0;
+    for (int a = 0; a < 3; ++a) {
+        const double v0 = t9[a], v1 = t9[a] + t9[3 + a], v2 = t9[a] + t9[6 + a];
+        lo[a] = fmin(v0, fmin(v1, v2));
+        hi[a] = fmax(v0, fmax(v1, v2));
+        ext = fmax(ext, hi[a] - lo[a]);
+        mag = fmax(mag, fmax(fabs(lo[a]), fabs(hi[a])));
+    }
+    const double pad = 1e-6 * ext + 1e-12 * mag;
+    for (int a = 0; a < 3; ++a) { lo[a] -= pad; hi[a] += pad; }
+}
+
+__global__ void k_permute_tris(const double* __restrict__ v0, const double* __restrict__ e1,
+                               const double* __restrict__ e2, const int32_t* __restrict__ tri_id,
+                               int32_t n, double* tri) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int32_t f = tri_id[i];
+        for (int a = 0; a < 3; ++a) {
+            tri[9 * (size_t)i + a] = v0[3 * (size_t)f + a];
+            tri[9 * (size_t)i + 3 + a] = e1[3 * (size_t)f + a];
+            tri[9 * (size_t)i + 6 + a] = e2[3 * (size_t)f + a];
+        }
+    }
+}
+
+__global__ void k_refit(BvhNode* nodes, const int32_t* __restrict__ parent,
+                        const int32_t* __restrict__ leaves, int32_t n_leaves, const double* tri,
+                        int32_t* visits) {
+    for (int32_t li = blockIdx.x * blockDim.x + threadIdx.x; li < n_leaves;
+         li += gridDim.x * blockDim.x) {
+        int32_t node = leaves[li];
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        const BvhNode leaf = nodes[node];
+        for (int i = 0; i < leaf.count; ++i) {
+            double a[3], b[3];
+            face_box_pad(tri + 9 * (size_t)(leaf.first + i), a, b);
+            for (int k = 0; k < 3; ++k) { lo[k] = fmin(lo[k], a[k]); hi[k] = fmax(hi[k], b[k]); }
+        }
+        for (int k = 0; k < 3; ++k) { nodes[node].lo[k] = lo[k]; nodes[node].hi[k] = hi[k]; }
+        while (true) {
+            const int32_t p = parent[node];
+            if (p < 0) break;
+            __threadfence();
+            if (atomicAdd(&visits[p], 1) == 0) break;      // sibling not done yet
+            __threadfence();
+            const int32_t c = nodes[p].first;
+            for (int k = 0; k < 3; ++k) {
+                const double l0 = __ldcg(&nodes[c].lo[k]), l1 = __ldcg(&nodes[c + 1].lo[k]);
+                const double h0 = __ldcg(&nodes[c].hi[k]), h1 = __ldcg(&nodes[c + 1].hi[k]);
+                nodes[p].lo[k] = fmin(l0, l1);
+                nodes[p].hi[k] = fmax(h0, h1);
+            }
+            node = p;
+        }
+    }
+}
+
 }  // namespace bvh

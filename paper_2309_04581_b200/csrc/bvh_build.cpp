@@ -187,36 +187,17 @@ BvhHost build_bvh(int64_t n_faces, const double* v0, const double* e1, const dou
         std::memcpy(&out.tri[9 * (size_t)i + 6], e2 + 3 * (size_t)f, 3 * sizeof(double));
         out.tri_id[i] = f;
     }
-    return out;
-}
-
-// Refit: new vertex data for the same faces; leaf order and topology kept.
-void refit_bvh(BvhHost& b, const double* v0, const double* e1, const double* e2) {
-    for (int32_t i = 0; i < b.n_faces; ++i) {
-        const int32_t f = b.tri_id[i];
-        std::memcpy(&b.tri[9 * (size_t)i], v0 + 3 * (size_t)f, 3 * sizeof(double));
-        std::memcpy(&b.tri[9 * (size_t)i + 3], e1 + 3 * (size_t)f, 3 * sizeof(double));
-        std::memcpy(&b.tri[9 * (size_t)i + 6], e2 + 3 * (size_t)f, 3 * sizeof(double));
-    }
-    // children always follow their parent in the array: sweep backwards
-    for (int64_t ni = (int64_t)b.nodes.size() - 1; ni >= 0; --ni) {
-        BvhNodeHost& nd = b.nodes[ni];
-        Box bx;
+    out.parent.assign(out.nodes.size(), -1);
+    for (size_t ni = 0; ni < out.nodes.size(); ++ni) {
+        const BvhNodeHost& nd = out.nodes[ni];
         if (nd.count > 0) {
-            for (int32_t i = nd.first; i < nd.first + nd.count; ++i) {
-                const double* t = &b.tri[9 * (size_t)i];
-                bx.grow(face_box(t, t + 3, t + 6));
-            }
+            out.leaves.push_back((int32_t)ni);
         } else {
-            for (int c = 0; c < 2; ++c) {
-                Box cbx;
-                const BvhNodeHost& ch = b.nodes[nd.first + c];
-                for (int a = 0; a < 3; ++a) { cbx.lo[a] = ch.lo[a]; cbx.hi[a] = ch.hi[a]; }
-                bx.grow(cbx);
-            }
+            out.parent[nd.first] = (int32_t)ni;
+            out.parent[nd.first + 1] = (int32_t)ni;
         }
-        for (int a = 0; a < 3; ++a) { nd.lo[a] = bx.lo[a]; nd.hi[a] = bx.hi[a]; }
     }
+    return out;
 }
 
 }  // namespace hrt

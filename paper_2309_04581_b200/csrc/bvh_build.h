@@ -18,9 +18,10 @@ struct BvhHost {
     std::vector<BvhNodeHost> nodes;
     std::vector<double> tri;        // leaf order, 9 doubles per face
     std::vector<int32_t> tri_id;    // leaf order -> global face id
+    std::vector<int32_t> parent;    // node -> parent (-1 at the root), for GPU refit
+    std::vector<int32_t> leaves;    // indices of leaf nodes
 };
 
 BvhHost build_bvh(int64_t n_faces, const double* v0, const double* e1, const double* e2);
-void refit_bvh(BvhHost& b, const double* v0, const double* e1, const double* e2);
 
 }  // namespace hrt

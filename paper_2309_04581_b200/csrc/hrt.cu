@@ -37,8 +37,17 @@ constexpr int64_t kBatchCap = int64_t(1) << 24;   // samples per march round
 
 }  // namespace
 
+struct RefitState {              // device side of a BVH's GPU refit
+    int32_t* parent = nullptr;
+    int32_t* leaves = nullptr;
+    int32_t* visits = nullptr;
+    double* src = nullptr;         // staging: v0 | e1 | e2 in global face order
+    int32_t n_leaves = 0;
+};
+
 struct hrt_handle {
     DevScene sc{};
+    RefitState rf, rfb;
     std::vector<void*> allocs;
     hrt::BvhHost bvh, blk;
     BvhNode* d_nodes = nullptr;
@@ -92,6 +101,37 @@ struct hrt_handle {
 };
 
 namespace {
+
+int setup_refit(hrt_handle* h, const hrt::BvhHost& b, RefitState& r) {
+    if (b.n_faces == 0) return HRT_OK;
+    int rc;
+    if ((rc = h->upload(b.parent.data(), b.parent.size(), &r.parent))) return rc;
+    if ((rc = h->upload(b.leaves.data(), b.leaves.size(), &r.leaves))) return rc;
+    if ((rc = h->alloc(b.nodes.size() * 4, reinterpret_cast<void**>(&r.visits)))) return rc;
+    if ((rc = h->alloc((size_t)b.n_faces * 9 * 8, reinterpret_cast<void**>(&r.src)))) return rc;
+    r.n_leaves = (int32_t)b.leaves.size();
+    return HRT_OK;
+}
+
+// K11: upload the new world-space faces, permute them into leaf order and
+// refit the boxes bottom-up on the device.
+int refit_gpu(hrt_handle* h, const hrt::BvhHost& b, RefitState& r, DevBvh& dev, const double* v0,
+              const double* e1, const double* e2) {
+    const size_t n3 = 3 * (size_t)b.n_faces;
+    CK(cudaMemcpy(r.src, v0, n3 * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(r.src + n3, e1, n3 * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(r.src + 2 * n3, e2, n3 * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemset(r.visits, 0, b.nodes.size() * 4));
+    const unsigned g1 = (unsigned)std::min<int64_t>((b.n_faces + 255) / 256, 148 * 16);
+    bvh::k_permute_tris<<<g1, 256>>>(r.src, r.src + n3, r.src + 2 * n3, dev.tri_id, b.n_faces,
+                                     const_cast<double*>(dev.tri));
+    CK(cudaGetLastError());
+    const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((r.n_leaves + 255) / 256, 148 * 16));
+    bvh::k_refit<<<g2, 256>>>(const_cast<BvhNode*>(dev.nodes), r.parent, r.leaves, r.n_leaves, dev.tri,
+                              r.visits);
+    CK(cudaGetLastError());
+    return HRT_OK;
+}
 
 int upload_bvh(hrt_handle* h, const hrt::BvhHost& b, DevBvh& out) {
     out.n_faces = b.n_faces;
@@ -314,29 +354,32 @@ int ensure_state(hrt_handle* h, int64_t paths) {
     const int64_t n = paths;
     const int64_t nb = std::min<int64_t>(n * kern::kRoundSamples, kBatchCap);
     const size_t dbl = (size_t)n * 8, i32 = (size_t)n * 4, f4 = (size_t)n * 16;
-    const size_t bytes = 16 * dbl + 12 * i32 + f4 + (size_t)nb * (16 + 4 + 16) + 64 * 4 + 1024;
-    CK(cudaMalloc(&h->arena, bytes));
-    char* p = static_cast<char*>(h->arena);
-    auto take = [&](size_t b) { char* r = p; p += (b + 255) & ~size_t(255); return r; };
-    auto take_d = [&]() { return reinterpret_cast<double*>(take(dbl)); };
-    auto take_i = [&]() { return reinterpret_cast<int32_t*>(take(i32)); };
-    PathState& s = h->ps;
-    s.ox = take_d(); s.oy = take_d(); s.oz = take_d();
-    s.dx = take_d(); s.dy = take_d(); s.dz = take_d();
-    s.Lr = take_d(); s.Lg = take_d(); s.Lb = take_d();
-    s.Tr = take_d(); s.Tg = take_d(); s.Tb = take_d();
-    s.Tm = take_d(); s.t_hit = take_d();
-    s.neval = take_i(); s.face = take_i(); s.pix = take_i(); s.smp = take_i();
-    s.queue[0] = take_i(); s.queue[1] = take_i();
-    kern::MarchState& m = h->ms;
-    m.s0 = take_d(); m.delta = take_d();
-    m.n = take_i(); m.k = take_i(); m.base = take_i(); m.cnt = take_i();
-    m.mq[0] = take_i(); m.mq[1] = take_i();
-    m.dir32 = reinterpret_cast<float4*>(take(f4));
-    m.in = reinterpret_cast<fws::SampleIn*>(take((size_t)nb * 16));
-    m.sk = reinterpret_cast<int32_t*>(take((size_t)nb * 4));
-    m.out = reinterpret_cast<float4*>(take((size_t)nb * 16));
-    s.counters = reinterpret_cast<int32_t*>(take(64 * 4));
+    // two passes over the same carve: size it, then assign the pointers
+    for (int pass = 0; pass < 2; ++pass) {
+        char* base = static_cast<char*>(h->arena);
+        size_t off = 0;
+        auto take = [&](size_t b) { char* r = base + off; off += (b + 255) & ~size_t(255); return r; };
+        auto take_d = [&]() { return reinterpret_cast<double*>(take(dbl)); };
+        auto take_i = [&]() { return reinterpret_cast<int32_t*>(take(i32)); };
+        PathState& s = h->ps;
+        s.ox = take_d(); s.oy = take_d(); s.oz = take_d();
+        s.dx = take_d(); s.dy = take_d(); s.dz = take_d();
+        s.Lr = take_d(); s.Lg = take_d(); s.Lb = take_d();
+        s.Tr = take_d(); s.Tg = take_d(); s.Tb = take_d();
+        s.Tm = take_d(); s.t_hit = take_d();
+        s.neval = take_i(); s.face = take_i(); s.pix = take_i(); s.smp = take_i();
+        s.queue[0] = take_i(); s.queue[1] = take_i();
+        kern::MarchState& m = h->ms;
+        m.s0 = take_d(); m.delta = take_d();
+        m.n = take_i(); m.k = take_i(); m.base = take_i(); m.cnt = take_i();
+        m.mq[0] = take_i(); m.mq[1] = take_i();
+        m.dir32 = reinterpret_cast<float4*>(take(f4));
+        m.in = reinterpret_cast<fws::SampleIn*>(take((size_t)nb * 16));
+        m.sk = reinterpret_cast<int32_t*>(take((size_t)nb * 4));
+        m.out = reinterpret_cast<float4*>(take((size_t)nb * 16));
+        s.counters = reinterpret_cast<int32_t*>(take(64 * 4));
+        if (pass == 0) CK(cudaMalloc(&h->arena, off));
+    }
     h->cap = n;
     h->batch_cap = nb;
     return HRT_OK;
@@ -467,6 +510,8 @@ int hrt_create(const hrt_scene_desc* d, hrt_handle** out) {
     h->blk = hrt::build_bvh(d->n_blockers, d->bv0, d->be1, d->be2);
     if ((rc = upload_bvh(h, h->bvh, sc.bvh))) return bail(rc);
     if ((rc = upload_bvh(h, h->blk, sc.blockers))) return bail(rc);
+    if ((rc = setup_refit(h, h->bvh, h->rf))) return bail(rc);
+    if ((rc = setup_refit(h, h->blk, h->rfb))) return bail(rc);
     double *normal, *emission;
     int32_t* mesh_of;
     if ((rc = h->upload(d->normal, 3 * (size_t)d->n_faces, &normal))) return bail(rc);
@@ -643,22 +688,16 @@ int hrt_render_host(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t 
 int hrt_refit(hrt_handle* h, const double* v0, const double* e1, const double* e2, const double* normal,
               const double* bv0, const double* be1, const double* be2) {
     if (!h) return fail(HRT_EINVAL, "null handle");
-    if (h->bvh.n_faces) {
-        hrt::refit_bvh(h->bvh, v0, e1, e2);
-        CK(cudaMemcpy(const_cast<BvhNode*>(h->sc.bvh.nodes), h->bvh.nodes.data(),
-                      h->bvh.nodes.size() * sizeof(BvhNode), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(const_cast<double*>(h->sc.bvh.tri), h->bvh.tri.data(), h->bvh.tri.size() * 8,
-                      cudaMemcpyHostToDevice));
+    int rc;
+    if (h->bvh.n_faces && v0 && e1 && e2) {
+        if ((rc = refit_gpu(h, h->bvh, h->rf, h->sc.bvh, v0, e1, e2))) return rc;
         if (normal)
             CK(cudaMemcpy(h->d_normal, normal, 3 * (size_t)h->bvh.n_faces * 8, cudaMemcpyHostToDevice));
     }
-    if (h->blk.n_faces && bv0) {
-        hrt::refit_bvh(h->blk, bv0, be1, be2);
-        CK(cudaMemcpy(const_cast<BvhNode*>(h->sc.blockers.nodes), h->blk.nodes.data(),
-                      h->blk.nodes.size() * sizeof(BvhNode), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(const_cast<double*>(h->sc.blockers.tri), h->blk.tri.data(), h->blk.tri.size() * 8,
-                      cudaMemcpyHostToDevice));
+    if (h->blk.n_faces && bv0 && be1 && be2) {
+        if ((rc = refit_gpu(h, h->blk, h->rfb, h->sc.blockers, bv0, be1, be2))) return rc;
     }
+    CK(cudaDeviceSynchronize());
     return HRT_OK;
 }
 
