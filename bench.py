@@ -294,8 +294,9 @@ def run_ours(args, rank, world, local):
     dev_ms = sum(s["step_ms"] for s in steps)
     samples = sum(s["nerf_samples"] for s in steps)
     paths = sum(s["paths"] for s in steps)
-    march_ms = sum(s["march_ms"] for s in steps)
-    march_n = sum(s["march_launches"] for s in steps)
+    march_ms = sum(s["field_ms"] for s in steps)
+    march_n = sum(s["field_launches"] for s in steps)
+    evaluated = sum(s["evaluated"] for s in steps)
     launches = sum(s["launches"] for s in steps)
     t = torch.tensor([dev_ms, samples, paths, march_ms, march_n, launches], dtype=torch.float64,
                      device=dev)
@@ -331,7 +332,7 @@ def run_ours(args, rank, world, local):
         hbm, tflops, peak_src = peaks()
         enc_bytes = 8 * field.n_levels * field.n_features * 4            # 1024 B / sample
         mlp_flop = 2 * (field.enc_dim * 64 + 64 * 16 + 31 * 64 + 64 * 64 + 64 * 3)
-        march_samples = samples                                            # rank-0 launches
+        march_samples = evaluated                                          # rank-0 field-engine evaluations
         achieved = march_samples * enc_bytes / (march_ms * 1e-3) / 1e9
         traffic = ncu_traffic()
         line = {
@@ -348,7 +349,7 @@ def run_ours(args, rank, world, local):
                        "wall_s_timed_region": t_wall},
             "gpu_launches": int(launches),
             "roofline": {
-                "bound": "hbm", "kernel": "k_march_neural<32,2> (encode + 5-layer tcgen05 MLP + composite)",
+                "bound": "hbm", "kernel": "fws::k_field_ws<32,2> (warp-specialized hash encode + 5-layer tcgen05 MLP, TMEM operands)",
                 "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                 "bytes_per_sample": enc_bytes, "launches": int(march_n),

@@ -69,6 +69,10 @@ struct hrt_handle {
     int64_t batch_cap = 0;
     int32_t* pinned = nullptr;
     int64_t rounds = 0;
+    int64_t io_cap = 0;
+    int32_t *io_pix = nullptr, *io_pix_host = nullptr;
+    double *io_out = nullptr, *io_out_host = nullptr;
+    cudaStream_t io_stream = nullptr;
     int n_timed = 0;
     int64_t launches = 0;
     uint32_t* occ_dev = nullptr;
@@ -97,6 +101,11 @@ struct hrt_handle {
         if (ev1) cudaEventDestroy(ev1);
         for (cudaEvent_t e : mev) if (e) cudaEventDestroy(e);
         if (pinned) cudaFreeHost(pinned);
+        if (io_pix) cudaFree(io_pix);
+        if (io_out) cudaFree(io_out);
+        if (io_pix_host) cudaFreeHost(io_pix_host);
+        if (io_out_host) cudaFreeHost(io_out_host);
+        if (io_stream) cudaStreamDestroy(io_stream);
     }
 };
 
@@ -385,6 +394,24 @@ int ensure_state(hrt_handle* h, int64_t paths) {
     return HRT_OK;
 }
 
+// Persistent host-path buffers (grow only): device pixel list / frame and
+// their pinned host staging copies.
+int ensure_io(hrt_handle* h, int64_t npx) {
+    if (npx <= h->io_cap) return HRT_OK;
+    if (h->io_pix) cudaFree(h->io_pix);
+    if (h->io_out) cudaFree(h->io_out);
+    if (h->io_pix_host) cudaFreeHost(h->io_pix_host);
+    if (h->io_out_host) cudaFreeHost(h->io_out_host);
+    const size_t n = (size_t)std::max<int64_t>(npx, 1);
+    CK(cudaMalloc(&h->io_pix, n * 4));
+    CK(cudaMalloc(&h->io_out, n * 24));
+    CK(cudaMallocHost(&h->io_pix_host, n * 4));
+    CK(cudaMallocHost(&h->io_out_host, n * 24));
+    if (!h->io_stream) CK(cudaStreamCreateWithFlags(&h->io_stream, cudaStreamNonBlocking));
+    h->io_cap = npx;
+    return HRT_OK;
+}
+
 int read_counter(hrt_handle* h, int idx, cudaStream_t st, int32_t* v) {
     CK(cudaMemcpyAsync(h->pinned, h->ps.counters + idx, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -668,20 +695,19 @@ int hrt_render_host(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t 
                     const int32_t* pixels, int64_t n_pixels, double* out, hrt_stats* stats) {
     if (!h || !cam || !out) return fail(HRT_EINVAL, "null argument");
     const int64_t npx = pixels ? n_pixels : (int64_t)cam->width * cam->height;
-    int32_t* dpix = nullptr;
-    double* dout = nullptr;
-    CK(cudaMalloc(&dout, (size_t)std::max<int64_t>(npx, 1) * 3 * 8));
-    if (pixels) {
-        CK(cudaMalloc(&dpix, (size_t)std::max<int64_t>(npx, 1) * 4));
-        CK(cudaMemcpy(dpix, pixels, (size_t)npx * 4, cudaMemcpyHostToDevice));
+    int rc;
+    if ((rc = ensure_io(h, npx))) return rc;
+    cudaStream_t st = h->io_stream;
+    if (pixels) {       // stage through pinned memory so the H2D is a true async DMA
+        std::memcpy(h->io_pix_host, pixels, (size_t)npx * 4);
+        CK(cudaMemcpyAsync(h->io_pix, h->io_pix_host, (size_t)npx * 4, cudaMemcpyHostToDevice, st));
     }
-    int rc = hrt_render(h, cam, spp, seed, mode, dpix, npx, dout, stats, nullptr);
+    rc = hrt_render(h, cam, spp, seed, mode, pixels ? h->io_pix : nullptr, npx, h->io_out, stats, st);
     if (rc == HRT_OK || rc == HRT_ENONFINITE) {
-        if (cudaMemcpy(out, dout, (size_t)npx * 3 * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
-            rc = fail(HRT_ECUDA, "copy of the frame failed");
+        CK(cudaMemcpyAsync(h->io_out_host, h->io_out, (size_t)npx * 24, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::memcpy(out, h->io_out_host, (size_t)npx * 24);
     }
-    cudaFree(dout);
-    if (dpix) cudaFree(dpix);
     return rc;
 }
 
