@@ -197,6 +197,21 @@ HRT_DEV void encode_level(const NeuralField& nf, const NeuralLevel& lv, float3 r
 // gathers in flight per thread: issue() computes the corner indices and
 // starts the 8 loads, finish() forms the weights and accumulates (same
 // arithmetic, same order as encode_level).
+#ifndef HRT_FINE_NOL1
+#define HRT_FINE_NOL1 0
+#endif
+#ifndef HRT_FINE_LEVEL_N
+#define HRT_FINE_LEVEL_N 512
+#endif
+constexpr bool kFineNoL1 = HRT_FINE_NOL1;
+constexpr int kFineLevelN = HRT_FINE_LEVEL_N;
+
+HRT_DEV float2 ld_na(const float2* p) {
+    float2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return v;
+}
+
 struct LevelLoads {
     LevelCoord c;
     float2 v[8];
@@ -215,10 +230,18 @@ HRT_DEV void level_issue(const NeuralField& nf, const NeuralLevel& lv, float3 re
     } else {
         const uint32_t hy0 = Y * kHashY, hy1 = hy0 + kHashY;
         const uint32_t hz0 = Z * kHashZ, hz1 = hz0 + kHashZ;
+        if (kFineNoL1 && lv.n >= kFineLevelN) {
+            // fine hashed levels have little L1 reuse: keep their fills out of L1
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-            g.v[k] = __ldg(base + (((X + (uint32_t)(k & 1)) ^ ((k & 2) ? hy1 : hy0) ^
-                                    ((k & 4) ? hz1 : hz0)) & nf.tmask));
+            for (int k = 0; k < 8; ++k)
+                g.v[k] = ld_na(base + (((X + (uint32_t)(k & 1)) ^ ((k & 2) ? hy1 : hy0) ^
+                                        ((k & 4) ? hz1 : hz0)) & nf.tmask));
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                g.v[k] = __ldg(base + (((X + (uint32_t)(k & 1)) ^ ((k & 2) ? hy1 : hy0) ^
+                                        ((k & 4) ? hz1 : hz0)) & nf.tmask));
+        }
     }
 }
 

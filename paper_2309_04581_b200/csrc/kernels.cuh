@@ -242,7 +242,10 @@ HRT_DEV int32_t dda_next(const NeuralField& nf, const DevField& f, d3 of, d3 df,
 //           the other march queue
 // The evaluated sample set and the compositing order equal the oracle's
 // per-sample march (oracle/tracer.py march), so parity is unchanged.
-constexpr int kRoundSamples = 32;
+#ifndef HRT_ROUND_SAMPLES
+#define HRT_ROUND_SAMPLES 32
+#endif
+constexpr int kRoundSamples = HRT_ROUND_SAMPLES;   // max midpoints per path per round
 
 struct MarchState {         // per path, valid while the path is marching
     double* s0;
