@@ -10,11 +10,15 @@ from paper_2309_04581_b200 import configs  # noqa: E402
 from paper_2309_04581_b200.renderer import Renderer  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+res = tuple(int(v) for v in sys.argv[2].split("x")) if len(sys.argv) > 2 else None
+spp = int(sys.argv[3]) if len(sys.argv) > 3 else None
 t0 = time.time()
-scene = configs.BUILDERS[cfg]()
+scene = configs.BUILDERS[cfg](res=res) if res and cfg in (3, 4) else configs.BUILDERS[cfg]()
+if spp:
+    scene.render.spp = spp
 r = Renderer(scene)
 print(f"cfg{cfg} setup {time.time() - t0:.2f}s", flush=True)
-for it in range(4):
+for it in range(int(sys.argv[4]) if len(sys.argv) > 4 else 4):
     torch.cuda.synchronize()
     t = time.time()
     out = r.render_pixels(scene.camera, scene.render.spp, 0)
