@@ -32,7 +32,7 @@ int fail(int code, const std::string& msg) {
 
 constexpr int64_t kMaxPaths = int64_t(1) << 20;   // paths per wavefront chunk
 constexpr int kThreads = 256;
-constexpr int kTimedLaunches = 256;
+constexpr int kTimedLaunches = 1024;
 constexpr int64_t kBatchCap = int64_t(1) << 24;   // samples per march round
 
 }  // namespace
@@ -64,7 +64,7 @@ struct hrt_handle {
     int32_t* trace = nullptr;
     int64_t trace_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    cudaEvent_t mev[2 * 256] = {};
+    cudaEvent_t mev[2 * 1024] = {};
     kern::MarchState ms{};
     int64_t batch_cap = 0;
     int32_t* pinned = nullptr;
@@ -386,6 +386,7 @@ int ensure_state(hrt_handle* h, int64_t paths) {
         m.in = reinterpret_cast<fws::SampleIn*>(take((size_t)nb * 16));
         m.sk = reinterpret_cast<int32_t*>(take((size_t)nb * 4));
         m.out = reinterpret_cast<float4*>(take((size_t)nb * 16));
+        m.shadow = reinterpret_cast<int32_t*>(take((size_t)nb * 4));
         s.counters = reinterpret_cast<int32_t*>(take(64 * 4));
         if (pass == 0) CK(cudaMalloc(&h->arena, off));
     }
@@ -441,6 +442,12 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
         if ((rc = field_ws(h, h->ms.in, nullptr, (int64_t)live * S, (int64_t)live * S, h->ms.dir32,
                            h->ms.out, 0, st)))
             return rc;
+        if (h->sc.em.n > 0) {
+            const int64_t rows = (int64_t)live * S;
+            kern::k_shadow<<<grid_for(h, rows), kThreads, 0, st>>>(a, h->ms, mc, rows);
+            CK(cudaGetLastError());
+            ++h->launches;
+        }
         kern::k_comp<<<gl, kThreads, 0, st>>>(a, h->ms, mc);
         CK(cudaGetLastError());
         h->launches += 3;

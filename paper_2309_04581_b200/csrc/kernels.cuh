@@ -157,12 +157,27 @@ HRT_DEV void store_acc(const PathState& s, int32_t p, const Acc& c) {
     s.neval[p] = c.neval;
 }
 
-// field.py:244-255 for one evaluated midpoint sample.
+// A shadow ray is cast for a midpoint only where it can contribute
+// (field.py:246-251: opacity > 0 and max(rgb) > 0).
+HRT_DEV bool needs_shadow(const DevScene& sc, double al, const double rgb[3]) {
+    return sc.em.n > 0 && al > 0.0 && fmax(fmax(rgb[0], rgb[1]), rgb[2]) > 0.0;
+}
+
+// field.py:244-255 for one evaluated midpoint sample with its mask m.
+HRT_DEV void composite_m(Acc& c, double al, const double rgb[3], double m) {
+    const double am = al * m;
+    for (int ch = 0; ch < 3; ++ch) c.L[ch] = c.L[ch] + (c.Ts[ch] * am) * rgb[ch];
+    const double keep = 1.0 - al;
+    for (int ch = 0; ch < 3; ++ch) c.Ts[ch] = c.Ts[ch] * keep;
+    c.T = c.T * keep;
+}
+
+// Same with the shadow ray traced inline (dense-grid plugin path).
 HRT_DEV void composite(const Args& a, Acc& c, double sigma, const double rgb[3], double delta,
                        d3 p, int32_t pix, int32_t smp, int32_t k) {
     const double al = 1.0 - exp(-sigma * delta);
     double m = 1.0;
-    if (a.sc.em.n > 0 && al > 0.0 && fmax(fmax(rgb[0], rgb[1]), rgb[2]) > 0.0) {
+    if (needs_shadow(a.sc, al, rgb)) {
         m = path::shadow_mask(a.sc, p, a.seed, pix, smp, a.bounce, k);
         atomicAdd(&a.ps.counters[C_SHADOW], 1);
     }
@@ -259,6 +274,7 @@ struct MarchState {         // per path, valid while the path is marching
     fws::SampleIn* in;      // batch
     int32_t* sk;            // midpoint index of each batch sample
     float4* out;            // (sigma, rgb) of each batch sample
+    int32_t* shadow;        // per batch sample: 0 visible / 1 + blocked emitter index
 };
 
 __global__ void k_seg(Args a, MarchState m) {
@@ -346,7 +362,6 @@ __global__ void k_comp(Args a, MarchState m, int32_t mcur) {
         const int32_t cnt = m.cnt[p];
         const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
         const Segment g{m.s0[p], m.delta[p], m.n[p]};
-        const int32_t pix = s.pix[p], smp = s.smp[p];
         bool stop = false;
         for (int32_t i = 0; i < cnt; ++i) {
             if (halted(a.sc, c)) { stop = true; break; }
@@ -354,10 +369,11 @@ __global__ void k_comp(Args a, MarchState m, int32_t mcur) {
             const int32_t k = m.sk[row];
             const float4 f = m.out[row];
             const double rgb[3] = {(double)f.y, (double)f.z, (double)f.w};
-            const d3 x = sample_point(o, d, g, k);
+            const double al = 1.0 - exp(-(double)f.x * g.delta);
+            const double mask = a.sc.em.n > 0 ? path::mask_of(a.sc, m.shadow[row]) : 1.0;
             c.neval += 1;
             ++done;
-            composite(a, c, (double)f.x, rgb, g.delta, x, pix, smp, k);
+            composite_m(c, al, rgb, mask);
             if (a.trace) {
                 const fws::SampleIn r = m.in[row];
                 int32_t c3[3];
@@ -372,6 +388,37 @@ __global__ void k_comp(Args a, MarchState m, int32_t mcur) {
     }
     if (done) atomicAdd(&a.ps.counters[C_SAMPLES], done);
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.ps.counters[C_EVALS], a.ps.counters[C_NS]);
+}
+
+// K3 over the batch: one thread per sample row (sample-major, so a warp
+// traces the shadow rays of 32 neighbouring pixels at the same step). Rows
+// that cannot contribute (opacity 0 or black) cast no ray, as in the
+// reference (field.py:246-251).
+__global__ void k_shadow(Args a, MarchState m, int32_t mcur, int64_t rows) {
+    const int32_t nq = a.ps.counters[C_MQ0 + mcur];
+    const PathState& s = a.ps;
+    int32_t cast = 0;
+    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < rows;
+         row += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t p = m.in[row].path;
+        if (p < 0) continue;
+        const float4 f = m.out[row];
+        const double rgb[3] = {(double)f.y, (double)f.z, (double)f.w};
+        const double delta = m.delta[p];
+        const double al = 1.0 - exp(-(double)f.x * delta);
+        int32_t code = 0;
+        if (needs_shadow(a.sc, al, rgb)) {
+            const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+            const Segment g{m.s0[p], delta, m.n[p]};
+            const int32_t k = m.sk[row];
+            code = path::shadow_code(a.sc, sample_point(o, d, g, k), a.seed, s.pix[p], s.smp[p],
+                                     a.bounce, k);
+            ++cast;
+        }
+        m.shadow[row] = code;
+    }
+    (void)nq;
+    if (cast) atomicAdd(&a.ps.counters[C_SHADOW], cast);
 }
 
 // Start of a march round: empty the batch and the next march queue.

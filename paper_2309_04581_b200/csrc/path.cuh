@@ -91,11 +91,12 @@ HRT_DEV double dense_sample(const DevField& f, d3 p, double rgb[3]) {
 }
 
 // ----------------------------------------------------------------- shadows
-// EmitterSet.sample + shadow_mask_batch (render.py:96-123) for one point.
-HRT_DEV double shadow_mask(const DevScene& sc, d3 p, uint64_t seed, int64_t pix, int64_t smp,
-                           int64_t bounce, int64_t lane) {
+// EmitterSet.sample + shadow_mask_batch (render.py:96-123) for one point:
+// 0 if the sampled emitter point is visible, else 1 + emitter index.
+HRT_DEV int32_t shadow_code(const DevScene& sc, d3 p, uint64_t seed, int64_t pix, int64_t smp,
+                            int64_t bounce, int64_t lane) {
     const DevEmitters& em = sc.em;
-    if (em.n == 0) return 1.0;
+    if (em.n == 0) return 0;
     const double u_pick = rng::uniform(seed, pix, smp, bounce, rng::LIGHT_PICK, lane);
     const double u1 = rng::uniform(seed, pix, smp, bounce, rng::LIGHT_U, lane);
     const double u2 = rng::uniform(seed, pix, smp, bounce, rng::LIGHT_V, lane);
@@ -115,8 +116,18 @@ HRT_DEV double shadow_mask(const DevScene& sc, d3 p, uint64_t seed, int64_t pix,
     const double safe = fmax(dist, 1e-12);
     const d3 dir = {delta.x / safe, delta.y / safe, delta.z / safe};
     const bool blocked = bvh::any_hit(sc.blockers, p, dir, sc.spawn_eps, dist * (1.0 - 1e-4));
-    if (!blocked) return 1.0;
-    return fmin(fmax(1.0 - em.r_src[idx], 0.02), 1.0);
+    return blocked ? idx + 1 : 0;
+}
+
+// Mask value of a shadow code: 1, or clip(1 - r_src, 0.02, 1) when blocked.
+HRT_DEV double mask_of(const DevScene& sc, int32_t code) {
+    if (code == 0) return 1.0;
+    return fmin(fmax(1.0 - sc.em.r_src[code - 1], 0.02), 1.0);
+}
+
+HRT_DEV double shadow_mask(const DevScene& sc, d3 p, uint64_t seed, int64_t pix, int64_t smp,
+                           int64_t bounce, int64_t lane) {
+    return mask_of(sc, shadow_code(sc, p, seed, pix, smp, bounce, lane));
 }
 
 // ------------------------------------------------------------------ BSDFs
