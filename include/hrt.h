@@ -131,7 +131,20 @@ typedef struct {
     int64_t launches;             /* kernels this library launched */
     int64_t evaluated;            /* field evaluations incl. speculative ones discarded by early-out */
     int64_t rounds;               /* march rounds (generate -> field -> composite) */
+    float stage_ms[8];            /* per-stage device time (HRT_STAGE_*), only after hrt_set_profile(h, 1) */
 } hrt_stats;
+
+/* Pipeline stages timed by hrt_set_profile (CUDA events around every launch). */
+enum {
+    HRT_STAGE_RAYGEN = 0,         /* k_raygen / k_load_rays */
+    HRT_STAGE_INTERSECT = 1,      /* closest hit (K2) */
+    HRT_STAGE_MARCH_GEN = 2,      /* segment setup + occupancy DDA sample generation (K4) */
+    HRT_STAGE_FIELD = 3,          /* hash encode + tcgen05 MLP field engine (K5/K6) */
+    HRT_STAGE_SHADOW = 4,         /* shadow any-hit of NeRF samples (K3) */
+    HRT_STAGE_COMPOSITE = 5,      /* transmittance compositing (K7), dense-grid march */
+    HRT_STAGE_SHADE = 6,          /* BSDF sample, spawn, compaction (K8) */
+    HRT_STAGE_ACCUMULATE = 7      /* per-pixel sum / spp (K9) */
+};
 
 const char* hrt_last_error(void);
 int hrt_version(void);
@@ -160,6 +173,10 @@ int hrt_trace_paths(hrt_handle* h, const double* o, const double* d, const int64
  * occupancy cell) in device memory, up to cap records; enabled for the
  * next hrt_render call only. */
 int hrt_set_trace(hrt_handle* h, int32_t* records, int64_t cap);
+
+/* Per-stage device timing of later hrt_render calls into hrt_stats.stage_ms
+ * (on != 0) or off (default). Measurement aid: adds one event pair per launch. */
+int hrt_set_profile(hrt_handle* h, int32_t on);
 
 /* New world-space face geometry (same topology; host pointers). */
 int hrt_refit(hrt_handle* h, const double* v0, const double* e1, const double* e2,

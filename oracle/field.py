@@ -16,9 +16,10 @@ unpinned, parity against this definition is what the GPU tests check):
   Corner c = (cx, cy, cz) = (c & 1, c >> 1 & 1, c >> 2) has weight
   (wx * wy) * wz with w = f or 1 - f, index dense  X + r*Y + r*r*Z (r = N_l+1)
   or hashed (X ^ Y*2654435761 ^ Z*805459861) & (T - 1) in uint32, and the
-  feature accumulates acc = fma(w, table[...], acc) over c = 0..7 in float32
-  from +0 (correctly rounded fused multiply-add; oracle/native.c pins it with
-  glibc fmaf, the GPU uses fma.rn.f32x2).
+  feature is acc_0 + acc_1 where acc_x accumulates fma(w, table[...], acc_x)
+  over the corners with cx = x in increasing c, in float32 from +0 (correctly
+  rounded fused multiply-add; oracle/native.c pins it with glibc fmaf, the
+  GPU uses fma.rn.f32x2 with the two x halves on the two lanes of a pair).
 * MLP: float16 operands (features, hidden activations, weights), products
   exact, sums here in float64 (GPU: float32 tensor-core accumulation), ReLU
   then round-to-nearest float16 between layers; sigma = exp(z[0]);

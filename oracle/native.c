@@ -28,18 +28,20 @@ void oracle_rotate_fma(int64_t n, const double *v, const double *rot, double *ou
 
 /*
  * Hash-grid corner accumulation of the neural field (definition in
- * oracle/field.py): per sample and feature, acc = fmaf(w_c, v_c, acc) over
- * the 8 corners in order, starting from +0. fmaf is correctly rounded, so
- * this pins the GPU's fma.rn.f32x2 accumulation bit for bit.
+ * oracle/field.py): per sample and feature, two chains
+ * acc_x = fmaf(w_c, v_c, acc_x) over the corners c with c & 1 == x in
+ * increasing c, from +0; feature = acc_0 + acc_1 (float add). fmaf is
+ * correctly rounded, so this pins the GPU's fma.rn.f32x2 accumulation (and
+ * its lane-pair split of the corners) bit for bit.
  *   w: n x 8, v: n x 8 x F, out: n x F (float32)
  */
 void oracle_corner_fma(int64_t n, int32_t F, const float *w, const float *v, float *out)
 {
     for (int64_t i = 0; i < n; ++i)
         for (int32_t j = 0; j < F; ++j) {
-            float acc = 0.0f;
+            float acc[2] = {0.0f, 0.0f};
             for (int k = 0; k < 8; ++k)
-                acc = fmaf(w[8 * i + k], v[(8 * i + k) * F + j], acc);
-            out[i * F + j] = acc;
+                acc[k & 1] = fmaf(w[8 * i + k], v[(8 * i + k) * F + j], acc[k & 1]);
+            out[i * F + j] = acc[0] + acc[1];
         }
 }

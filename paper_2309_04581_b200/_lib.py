@@ -75,10 +75,16 @@ class Stats(ctypes.Structure):
                 ("trace_records", ctypes.c_int64), ("ms", ctypes.c_float),
                 ("field_ms", ctypes.c_float), ("field_launches", ctypes.c_int32),
                 ("launches", ctypes.c_int64), ("evaluated", ctypes.c_int64),
-                ("rounds", ctypes.c_int64)]
+                ("rounds", ctypes.c_int64), ("stage_ms", ctypes.c_float * 8)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["stage_ms"] = dict(zip(STAGES, list(self.stage_ms)))
+        return d
+
+
+# hrt.h HRT_STAGE_* order
+STAGES = ("raygen", "intersect", "march_gen", "field", "shadow", "composite", "shade", "accumulate")
 
 
 # name -> (restype, argtypes); this list is what include/hrt.h declares.
@@ -95,6 +101,7 @@ SIGNATURES = {
     "hrt_trace_paths": (ctypes.c_int, [vp, vp, vp, vp, vp, ctypes.c_int64, ctypes.c_uint64,
                                        ctypes.c_int32, vp, vp]),
     "hrt_set_trace": (ctypes.c_int, [vp, vp, ctypes.c_int64]),
+    "hrt_set_profile": (ctypes.c_int, [vp, ctypes.c_int32]),
     "hrt_refit": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "hrt_field_sample": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, vp]),
     "hrt_field_encode": (ctypes.c_int, [vp, vp, ctypes.c_int64, vp, vp, vp]),

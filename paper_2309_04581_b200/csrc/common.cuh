@@ -107,6 +107,8 @@ struct NeuralField {
     uint32_t tmask;
     NeuralLevel lv[kMaxLevels];
     const float* table;
+    unsigned long long tex;  // texture object over `table` (F-wide texels), fine-level gathers
+    int32_t tex_from;        // levels >= tex_from gather through the TEX pipe
     const uint8_t* wpack;   // UMMA B-operand images of the 5 layers, back to back
     int32_t occ_res;
     float occ_scale[3];
@@ -151,11 +153,19 @@ struct PathState {
     int32_t* pix;                             // pixel id of the path
     int32_t* smp;                             // sample index of the path
     int32_t* queue[2];                        // alive path ids, ping-pong
-    int32_t* counters;                        // [0],[1] queue sizes; [2] fetch cursor; [3..] stats
+    int32_t* counters;                        // [0],[1] queue sizes; [2] fetch cursor; [3..] per-round
+    unsigned long long* stats;                // whole-call totals (S_*), 64-bit: a 4K x 64 spp
+                                              // frame evaluates ~1e11 NeRF samples
 };
 
-enum Counter { C_Q0 = 0, C_Q1 = 1, C_FETCH = 2, C_SAMPLES = 3, C_SHADOW = 4, C_SEGMENTS = 5,
-               C_NONFINITE = 6, C_TRACE = 7, C_MQ0 = 8, C_MQ1 = 9, C_NS = 10, C_EVALS = 11,
+enum Stat { S_SAMPLES = 0, S_SHADOW = 1, S_SEGMENTS = 2, S_EVALS = 3, S_COUNT = 8 };
+
+HRT_DEV void stat_add(unsigned long long* stats, int which, long long v) {
+    atomicAdd(stats + which, (unsigned long long)v);
+}
+
+enum Counter { C_Q0 = 0, C_Q1 = 1, C_FETCH = 2,
+               C_NONFINITE = 6, C_TRACE = 7, C_MQ0 = 8, C_MQ1 = 9, C_NS = 10,
                C_COUNT = 16 };
 
 HRT_DEV d3 field_point(const DevField& f, d3 p) {

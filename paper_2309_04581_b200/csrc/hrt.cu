@@ -34,6 +34,14 @@ constexpr int64_t kMaxPaths = int64_t(1) << 20;   // paths per wavefront chunk
 constexpr int kThreads = 256;
 constexpr int kTimedLaunches = 1024;
 constexpr int64_t kBatchCap = int64_t(1) << 24;   // samples per march round
+#ifndef HRT_TEX_LEVELS
+#define HRT_TEX_LEVELS 8
+#endif
+constexpr int kTexLevels = HRT_TEX_LEVELS;        // finest levels gathered via TEX
+#ifndef HRT_TILED_FRAME
+#define HRT_TILED_FRAME 1
+#endif
+constexpr bool kTiledFrame = HRT_TILED_FRAME;      // full frames walk 16x16 pixel tiles
 
 }  // namespace
 
@@ -77,6 +85,13 @@ struct hrt_handle {
     int64_t launches = 0;
     uint32_t* occ_dev = nullptr;
     int64_t occ_words = 0;
+    unsigned long long tex = 0;
+    // hrt_set_profile: event pair per launch, folded into stage_ms
+    bool prof = false;
+    std::vector<cudaEvent_t> pev;
+    std::vector<int> pstage;
+    int pn = 0;
+    double stage_ms[8] = {};
 
     template <class T>
     int upload(const T* src, size_t n, T** dst) {
@@ -100,12 +115,14 @@ struct hrt_handle {
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         for (cudaEvent_t e : mev) if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : pev) cudaEventDestroy(e);
         if (pinned) cudaFreeHost(pinned);
         if (io_pix) cudaFree(io_pix);
         if (io_out) cudaFree(io_out);
         if (io_pix_host) cudaFreeHost(io_pix_host);
         if (io_out_host) cudaFreeHost(io_out_host);
         if (io_stream) cudaStreamDestroy(io_stream);
+        if (tex) cudaDestroyTextureObject(tex);
     }
 };
 
@@ -223,6 +240,22 @@ int setup_field(hrt_handle* h, const hrt_field_desc& fd) {
         float* table;
         if ((rc = h->upload(tab.data(), tab.size(), &table))) return rc;
         nf.table = table;
+        {   // texture view of the table: the finest (incoherent) levels gather through the
+            // TEX pipe of L1TEX, the rest through LSU, splitting the data-stage load
+            cudaResourceDesc rd{};
+            rd.resType = cudaResourceTypeLinear;
+            rd.res.linear.devPtr = table;
+            rd.res.linear.desc = F == 2 ? cudaCreateChannelDesc<float2>() : cudaCreateChannelDesc<float4>();
+            rd.res.linear.sizeInBytes = tab.size() * sizeof(float);
+            cudaTextureDesc td{};
+            td.readMode = cudaReadModeElementType;
+            td.filterMode = cudaFilterModePoint;
+            cudaTextureObject_t to = 0;
+            CK(cudaCreateTextureObject(&to, &rd, &td, nullptr));
+            h->tex = to;
+            nf.tex = to;
+            nf.tex_from = std::max(0, L - kTexLevels);
+        }
         const nerf::WOff W = nerf::woff(E);
         std::vector<uint8_t> img(W.total);
         pack_layer(fd.w_density1, E, 64, E, 64, img.data() + W.d1);
@@ -388,6 +421,7 @@ int ensure_state(hrt_handle* h, int64_t paths) {
         m.out = reinterpret_cast<float4*>(take((size_t)nb * 16));
         m.shadow = reinterpret_cast<int32_t*>(take((size_t)nb * 4));
         s.counters = reinterpret_cast<int32_t*>(take(64 * 4));
+        s.stats = reinterpret_cast<unsigned long long*>(take(S_COUNT * 8));
         if (pass == 0) CK(cudaMalloc(&h->arena, off));
     }
     h->cap = n;
@@ -420,13 +454,38 @@ int read_counter(hrt_handle* h, int idx, cudaStream_t st, int32_t* v) {
     return HRT_OK;
 }
 
+// ---- stage profiler (hrt_set_profile): pbeg/pend bracket one launch
+constexpr int kProfPairs = 4096;
+
+void prof_fold(hrt_handle* h, cudaStream_t st) {
+    if (!h->prof || h->pn == 0) return;
+    cudaStreamSynchronize(st);
+    for (int i = 0; i < h->pn; ++i) {
+        float x = 0.f;
+        cudaEventElapsedTime(&x, h->pev[2 * i], h->pev[2 * i + 1]);
+        h->stage_ms[h->pstage[i]] += x;
+    }
+    h->pn = 0;
+}
+inline void pbeg(hrt_handle* h, cudaStream_t st) {
+    if (h->prof) cudaEventRecord(h->pev[2 * h->pn], st);
+}
+inline void pend(hrt_handle* h, int stage, cudaStream_t st) {
+    if (!h->prof) return;
+    cudaEventRecord(h->pev[2 * h->pn + 1], st);
+    h->pstage[h->pn++] = stage;
+    if (h->pn == kProfPairs) prof_fold(h, st);
+}
+
 // NeRF march of every alive path of this bounce: k_seg, then rounds of
 // k_gen -> k_field_ws -> k_comp until no path has midpoints left.
 int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream_t st) {
     const unsigned g = grid_for(h, n_paths);
+    pbeg(h, st);
     kern::k_round_reset<<<1, 1, 0, st>>>(h->ps.counters, 0);
     kern::k_seg<<<g, kThreads, 0, st>>>(a, h->ms);
     CK(cudaGetLastError());
+    pend(h, HRT_STAGE_MARCH_GEN, st);
     h->launches += 2;
     int32_t live = 0;
     int rc;
@@ -436,20 +495,29 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
         const int32_t S = (int32_t)std::max<int64_t>(
             1, std::min<int64_t>(kern::kRoundSamples, h->batch_cap / live));
         const unsigned gl = grid_for(h, live);
+        pbeg(h, st);
         kern::k_round_reset<<<1, 1, 0, st>>>(h->ps.counters, mc ^ 1);
         kern::k_gen<<<gl, kThreads, 0, st>>>(a, h->ms, mc, S);
         CK(cudaGetLastError());
+        pend(h, HRT_STAGE_MARCH_GEN, st);
+        pbeg(h, st);
         if ((rc = field_ws(h, h->ms.in, nullptr, (int64_t)live * S, (int64_t)live * S, h->ms.dir32,
                            h->ms.out, 0, st)))
             return rc;
+        pend(h, HRT_STAGE_FIELD, st);
         if (h->sc.em.n > 0) {
             const int64_t rows = (int64_t)live * S;
+            pbeg(h, st);
             kern::k_shadow<<<grid_for(h, rows), kThreads, 0, st>>>(a, h->ms, mc, rows);
             CK(cudaGetLastError());
+            pend(h, HRT_STAGE_SHADOW, st);
             ++h->launches;
         }
-        kern::k_comp<<<gl, kThreads, 0, st>>>(a, h->ms, mc);
+        pbeg(h, st);
+        if (a.trace) kern::k_comp<true><<<gl, kThreads, 0, st>>>(a, h->ms, mc);
+        else kern::k_comp<false><<<gl, kThreads, 0, st>>>(a, h->ms, mc);
         CK(cudaGetLastError());
+        pend(h, HRT_STAGE_COMPOSITE, st);
         h->launches += 3;
         ++h->rounds;
         if ((rc = read_counter(h, C_MQ0 + (mc ^ 1), st, &live))) return rc;
@@ -460,8 +528,10 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
 
 int march(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream_t st) {
     if (h->sc.field.kind == HRT_FIELD_DENSE) {
+        pbeg(h, st);
         kern::k_march_dense<<<grid_for(h, n_paths), kThreads, 0, st>>>(a);
         CK(cudaGetLastError());
+        pend(h, HRT_STAGE_COMPOSITE, st);
         ++h->launches;
         return HRT_OK;
     }
@@ -486,12 +556,16 @@ int run_bounces(hrt_handle* h, kern::Args& a, int64_t paths, int mode, cudaStrea
     for (int b = 1; b <= h->sc.n_bounces; ++b) {
         a.bounce = b;
         a.cur = (b - 1) & 1;
+        pbeg(h, st);
         kern::k_reset_queue<<<1, 1, 0, st>>>(h->ps.counters, a.cur ^ 1);
         kern::k_intersect<<<g, kThreads, 0, st>>>(a);
         CK(cudaGetLastError());
+        pend(h, HRT_STAGE_INTERSECT, st);
         if (field && mode == HRT_MODE_HYBRID && (rc = march(h, a, paths, st))) return rc;
+        pbeg(h, st);
         kern::k_shade<<<g, kThreads, 0, st>>>(a);
         CK(cudaGetLastError());
+        pend(h, HRT_STAGE_SHADE, st);
         h->launches += 3;
     }
     return HRT_OK;
@@ -599,6 +673,17 @@ int hrt_set_trace(hrt_handle* h, int32_t* records, int64_t cap) {
     return HRT_OK;
 }
 
+int hrt_set_profile(hrt_handle* h, int32_t on) {
+    if (!h) return fail(HRT_EINVAL, "null handle");
+    if (on && h->pev.empty()) {
+        h->pev.resize(2 * kProfPairs);
+        h->pstage.resize(kProfPairs);
+        for (cudaEvent_t& e : h->pev) CK(cudaEventCreate(&e));
+    }
+    h->prof = on != 0;
+    return HRT_OK;
+}
+
 int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed, int32_t mode,
                const int32_t* pixels, int64_t n_pixels, double* out, hrt_stats* stats, void* stream) {
     if (!h || !cam || !out) return fail(HRT_EINVAL, "null argument");
@@ -611,9 +696,12 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
     int rc;
     if ((rc = ensure_state(h, std::min<int64_t>(total_pix, chunk_pix) * spp))) return rc;
     CK(cudaMemsetAsync(h->ps.counters, 0, 64 * 4, st));
+    CK(cudaMemsetAsync(h->ps.stats, 0, S_COUNT * 8, st));
     h->n_timed = 0;
     h->launches = 0;
     h->rounds = 0;
+    h->pn = 0;
+    for (double& x : h->stage_ms) x = 0.0;
     CK(cudaEventRecord(h->ev0, st));
     for (int64_t p0 = 0; p0 < total_pix; p0 += chunk_pix) {
         const int64_t np = std::min(chunk_pix, total_pix - p0);
@@ -630,27 +718,35 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
         a.seed = seed;
         a.out = out;
         a.out_offset = p0;
+        a.tiled = (!pixels && kTiledFrame) ? 1 : 0;
         a.trace = h->trace;
         a.trace_cap = h->trace_cap;
+        pbeg(h, st);
         kern::k_raygen<<<grid_for(h, paths), kThreads, 0, st>>>(a);
         CK(cudaGetLastError());
+        pend(h, HRT_STAGE_RAYGEN, st);
         h->launches += 2;   // raygen + accumulate
         if ((rc = run_bounces(h, a, paths, mode, st))) return rc;
+        pbeg(h, st);
         kern::k_accumulate<<<grid_for(h, np), kThreads, 0, st>>>(a);
         CK(cudaGetLastError());
+        pend(h, HRT_STAGE_ACCUMULATE, st);
     }
+    prof_fold(h, st);
     CK(cudaEventRecord(h->ev1, st));
     h->trace = nullptr;
     int32_t ctr[64];
+    unsigned long long tot[S_COUNT];
     CK(cudaMemcpyAsync(ctr, h->ps.counters, sizeof(ctr), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(tot, h->ps.stats, sizeof(tot), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (stats) {
         stats->paths = total_pix * spp;
-        stats->nerf_samples = ctr[C_SAMPLES];
-        stats->shadow_rays = ctr[C_SHADOW];
-        stats->bounce_rays = ctr[C_SEGMENTS];
+        stats->nerf_samples = (int64_t)tot[S_SAMPLES];
+        stats->shadow_rays = (int64_t)tot[S_SHADOW];
+        stats->bounce_rays = (int64_t)tot[S_SEGMENTS];
         stats->trace_records = ctr[C_TRACE];
-        stats->evaluated = ctr[C_EVALS];
+        stats->evaluated = (int64_t)tot[S_EVALS];
         stats->rounds = h->rounds;
         float ms = 0.f;
         cudaEventElapsedTime(&ms, h->ev0, h->ev1);
@@ -664,6 +760,7 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
         stats->field_ms = mms;
         stats->field_launches = h->n_timed;
         stats->launches = h->launches;
+        for (int i = 0; i < 8; ++i) stats->stage_ms[i] = (float)h->stage_ms[i];
     }
     if (ctr[C_NONFINITE] != 0) return fail(HRT_ENONFINITE, "non-finite or negative radiance in frame");
     return HRT_OK;
@@ -680,6 +777,7 @@ int hrt_trace_paths(hrt_handle* h, const double* o, const double* d, const int64
     int rc;
     if ((rc = ensure_state(h, n))) return rc;
     CK(cudaMemsetAsync(h->ps.counters, 0, 64 * 4, st));
+    CK(cudaMemsetAsync(h->ps.stats, 0, S_COUNT * 8, st));
     kern::Args a{};
     a.sc = h->sc;
     a.ps = h->ps;

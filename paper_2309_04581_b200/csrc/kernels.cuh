@@ -28,9 +28,16 @@ struct Args {
     int32_t volume;          // degenerate tracer B: no surfaces, t_hit = inf
     double* out;             // (n_slots, 3) device output
     int64_t out_offset;      // slot offset in `out`
+    int32_t tiled;           // full frame: slots walk 16x16 pixel tiles, out is raster
     int32_t* trace;          // optional (path, bounce, k, cell) records
     int64_t trace_cap;
 };
+
+// One of a two-entry pointer array in a kernel parameter. A plain
+// arr[runtime index] makes the compiler copy the whole parameter struct to
+// local memory (ncu: STL of every field at kernel entry).
+template <class T>
+HRT_DEV T* pick(T* const (&arr)[2], int32_t i) { return i ? arr[1] : arr[0]; }
 
 // Warp-aggregated reservation of `n` slots on a device counter.
 HRT_DEV int32_t reserve(int32_t* ctr) {
@@ -41,12 +48,35 @@ HRT_DEV int32_t reserve(int32_t* ctr) {
     return base + (int32_t)g.thread_rank();
 }
 
+// Full-frame slot order: 16x16 pixel tiles in raster tile order, raster
+// inside a tile (edge tiles partial). Consecutive paths are then a compact
+// 2-D pixel block, so a 128-row sample tile of the field engine gathers a
+// 16x8 footprint instead of a 128x1 strip (L1 reuse of the mid hash levels).
+// Paths are keyed by pixel, so the order never changes a result.
+constexpr int kTile = 16;
+HRT_DEV int64_t tiled_pixel(int64_t slot, int32_t W, int32_t H) {
+    const int64_t band = (int64_t)W * kTile;
+    const int64_t ty = slot / band;
+    const int64_t rem = slot - ty * band;
+    const int64_t ht = min((int64_t)kTile, (int64_t)H - ty * kTile);
+    const int64_t tx = rem / (kTile * ht);
+    const int64_t r2 = rem - tx * kTile * ht;
+    const int64_t wt = min((int64_t)kTile, (int64_t)W - tx * kTile);
+    return (ty * kTile + r2 / wt) * W + tx * kTile + r2 % wt;
+}
+
+HRT_DEV int64_t slot_pixel(const Args& a, int64_t slot) {
+    if (a.pixels) return a.pixels[slot];
+    const int64_t s = a.pixel_base + slot;
+    return a.tiled ? tiled_pixel(s, a.cam.width, a.cam.height) : s;
+}
+
 __global__ void k_raygen(Args a) {
     const int64_t n = a.n_slots * a.spp;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
         const int64_t slot = p / a.spp, smp = p % a.spp;
-        const int64_t pix = a.pixels ? a.pixels[slot] : a.pixel_base + slot;
+        const int64_t pix = slot_pixel(a, slot);
         d3 o, d;
         path::primary_ray(a.cam, pix, smp, a.seed, a.strat, o, d);
         PathState& s = a.ps;
@@ -96,9 +126,9 @@ __global__ void k_load_rays(Args a, const double* o, const double* d, const int6
 // K2: nearest hit of every alive path, t in (0, inf] (render.py:217).
 __global__ void k_intersect(Args a) {
     const int32_t n = a.ps.counters[a.cur];
-    const int32_t* q = a.ps.queue[a.cur];
+    const int32_t* q = pick(a.ps.queue, a.cur);
     PathState& s = a.ps;
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&s.counters[C_SEGMENTS], n);
+    if (blockIdx.x == 0 && threadIdx.x == 0) stat_add(s.stats, S_SEGMENTS, n);
     for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
         const int32_t p = q[j];
         double t = INFINITY;
@@ -179,7 +209,7 @@ HRT_DEV void composite(const Args& a, Acc& c, double sigma, const double rgb[3],
     double m = 1.0;
     if (needs_shadow(a.sc, al, rgb)) {
         m = path::shadow_mask(a.sc, p, a.seed, pix, smp, a.bounce, k);
-        atomicAdd(&a.ps.counters[C_SHADOW], 1);
+        stat_add(a.ps.stats, S_SHADOW, 1);
     }
     const double am = al * m;
     for (int ch = 0; ch < 3; ++ch) c.L[ch] = c.L[ch] + (c.Ts[ch] * am) * rgb[ch];
@@ -198,7 +228,7 @@ HRT_DEV bool halted(const DevScene& sc, const Acc& c) {
 // through every midpoint of its segment, as march_arrays does.
 __global__ void k_march_dense(Args a) {
     const int32_t n = a.ps.counters[a.cur];
-    const int32_t* q = a.ps.queue[a.cur];
+    const int32_t* q = pick(a.ps.queue, a.cur);
     const PathState& s = a.ps;
     for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
         const int32_t p = q[j];
@@ -219,7 +249,7 @@ __global__ void k_march_dense(Args a) {
             composite(a, c, sigma, rgb, g.delta, x, pix, smp, k);
         }
         store_acc(s, p, c);
-        atomicAdd(&a.ps.counters[C_SAMPLES], evals);
+        stat_add(a.ps.stats, S_SAMPLES, evals);
     }
 }
 
@@ -279,7 +309,7 @@ struct MarchState {         // per path, valid while the path is marching
 
 __global__ void k_seg(Args a, MarchState m) {
     const int32_t n = a.ps.counters[a.cur];
-    const int32_t* q = a.ps.queue[a.cur];
+    const int32_t* q = pick(a.ps.queue, a.cur);
     const PathState& s = a.ps;
     for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
         const int32_t p = q[j];
@@ -298,7 +328,7 @@ __global__ void k_seg(Args a, MarchState m) {
 
 __global__ void k_gen(Args a, MarchState m, int32_t mcur, int32_t S) {
     const int32_t nq = a.ps.counters[C_MQ0 + mcur];
-    const int32_t* q = m.mq[mcur];
+    const int32_t* q = pick(m.mq, mcur);
     const PathState& s = a.ps;
     const DevField& fld = a.sc.field;
     const NeuralField& nf = fld.nf;
@@ -347,10 +377,19 @@ __global__ void k_gen(Args a, MarchState m, int32_t mcur, int32_t S) {
     }
 }
 
-__global__ void k_comp(Args a, MarchState m, int32_t mcur) {
+#ifndef HRT_COMP_BATCH
+#define HRT_COMP_BATCH 4
+#endif
+constexpr int32_t kCompBatch = HRT_COMP_BATCH;
+
+#ifndef HRT_COMP_MINB
+#define HRT_COMP_MINB 1
+#endif
+template <bool kTrace>
+__global__ void __launch_bounds__(256, HRT_COMP_MINB) k_comp(Args a, MarchState m, int32_t mcur) {
     const int32_t nq = a.ps.counters[C_MQ0 + mcur];
-    const int32_t* q = m.mq[mcur];
-    int32_t* next = m.mq[mcur ^ 1];
+    const int32_t* q = pick(m.mq, mcur);
+    int32_t* next = pick(m.mq, mcur ^ 1);
     int32_t* next_n = &a.ps.counters[C_MQ0 + (mcur ^ 1)];
     const PathState& s = a.ps;
     const NeuralField& nf = a.sc.field.nf;
@@ -363,18 +402,33 @@ __global__ void k_comp(Args a, MarchState m, int32_t mcur) {
         const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
         const Segment g{m.s0[p], m.delta[p], m.n[p]};
         bool stop = false;
-        for (int32_t i = 0; i < cnt; ++i) {
+        // rows are read kCompBatch at a time ahead of the (sequential) halt
+        // test, so a path waits one memory latency per batch, not per sample
+        for (int32_t i0 = 0; i0 < cnt && !stop; i0 += kCompBatch) {
+            float4 fb[kCompBatch];
+            int32_t cb[kCompBatch];
+#pragma unroll
+            for (int32_t u = 0; u < kCompBatch; ++u) {
+                const int64_t row = (int64_t)(i0 + u) * nq + j;
+                const bool in = i0 + u < cnt;
+                fb[u] = in ? __ldcs(&m.out[row]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                cb[u] = (in && a.sc.em.n > 0) ? __ldcs(&m.shadow[row]) : 0;
+            }
+#pragma unroll
+            for (int32_t u = 0; u < kCompBatch; ++u) {
+            const int32_t i = i0 + u;
+            if (i >= cnt) break;
             if (halted(a.sc, c)) { stop = true; break; }
             const int64_t row = (int64_t)i * nq + j;
-            const int32_t k = m.sk[row];
-            const float4 f = m.out[row];
+            const float4 f = fb[u];
             const double rgb[3] = {(double)f.y, (double)f.z, (double)f.w};
             const double al = 1.0 - exp(-(double)f.x * g.delta);
-            const double mask = a.sc.em.n > 0 ? path::mask_of(a.sc, m.shadow[row]) : 1.0;
+            const double mask = path::mask_of(a.sc, cb[u]);
             c.neval += 1;
             ++done;
             composite_m(c, al, rgb, mask);
-            if (a.trace) {
+            if (kTrace) {
+                const int32_t k = m.sk[row];
                 const fws::SampleIn r = m.in[row];
                 int32_t c3[3];
                 const int32_t cell = nerf::occ_cell(nf, mk(r.x, r.y, r.z), c3);
@@ -382,12 +436,13 @@ __global__ void k_comp(Args a, MarchState m, int32_t mcur) {
                 if (slot < a.trace_cap)
                     reinterpret_cast<int4*>(a.trace)[slot] = make_int4(p, a.bounce, k, cell);
             }
+            }
         }
         store_acc(s, p, c);
         if (!stop && !halted(a.sc, c) && m.k[p] < g.n) next[reserve(next_n)] = p;
     }
-    if (done) atomicAdd(&a.ps.counters[C_SAMPLES], done);
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.ps.counters[C_EVALS], a.ps.counters[C_NS]);
+    if (done) stat_add(a.ps.stats, S_SAMPLES, done);
+    if (blockIdx.x == 0 && threadIdx.x == 0) stat_add(a.ps.stats, S_EVALS, a.ps.counters[C_NS]);
 }
 
 // K3 over the batch: one thread per sample row (sample-major, so a warp
@@ -418,7 +473,7 @@ __global__ void k_shadow(Args a, MarchState m, int32_t mcur, int64_t rows) {
         m.shadow[row] = code;
     }
     (void)nq;
-    if (cast) atomicAdd(&a.ps.counters[C_SHADOW], cast);
+    if (cast) stat_add(a.ps.stats, S_SHADOW, cast);
 }
 
 // Start of a march round: empty the batch and the next march queue.
@@ -430,8 +485,8 @@ __global__ void k_round_reset(int32_t* counters, int32_t next_mq) {
 // K8: hit shading, BSDF sample, spawn, compaction (render.py:221-244).
 __global__ void k_shade(Args a) {
     const int32_t n = a.ps.counters[a.cur];
-    const int32_t* q = a.ps.queue[a.cur];
-    int32_t* next = a.ps.queue[a.cur ^ 1];
+    const int32_t* q = pick(a.ps.queue, a.cur);
+    int32_t* next = pick(a.ps.queue, a.cur ^ 1);
     int32_t* next_n = &a.ps.counters[a.cur ^ 1];
     const PathState& s = a.ps;
     const DevScene& sc = a.sc;
@@ -505,7 +560,7 @@ __global__ void k_accumulate(Args a) {
             acc[1] = acc[1] + s.Lg[p];
             acc[2] = acc[2] + s.Lb[p];
         }
-        double* o = a.out + 3 * (a.out_offset + slot);
+        double* o = a.out + 3 * (a.tiled ? slot_pixel(a, slot) : a.out_offset + slot);
         bool bad = false;
         for (int ch = 0; ch < 3; ++ch) {
             const double v = acc[ch] / (double)a.spp;

@@ -155,6 +155,10 @@ class Renderer:
         _lib.check(rc, "hrt_intersect")
         return t, f
 
+    def set_profile(self, on=True):
+        """Per-stage device timing of later renders (last_stats['stage_ms'])."""
+        _lib.check(self.lib.hrt_set_profile(self.handle, int(bool(on))), "hrt_set_profile")
+
     def set_trace(self, records, cap):
         _lib.check(self.lib.hrt_set_trace(self.handle, _dptr(records), int(cap)), "hrt_set_trace")
 

@@ -17,6 +17,7 @@ scene = configs.BUILDERS[cfg](res=res) if res and cfg in (3, 4) else configs.BUI
 if spp:
     scene.render.spp = spp
 r = Renderer(scene)
+r.set_profile(True)
 print(f"cfg{cfg} setup {time.time() - t0:.2f}s", flush=True)
 for it in range(int(sys.argv[4]) if len(sys.argv) > 4 else 4):
     torch.cuda.synchronize()
@@ -30,3 +31,4 @@ for it in range(int(sys.argv[4]) if len(sys.argv) > 4 else 4):
           f"Mrays/s {s['paths']/s['ms']*1e3/1e6:.2f} mean {out.mean().item():.4f} | field {s['field_ms']:.1f} ms "
           f"x{s['field_launches']} evaluated {s['evaluated']:,} rounds {s['rounds']} launches {s['launches']}",
           flush=True)
+    print("   stages ms: " + " ".join(f"{k}={v:.1f}" for k, v in s["stage_ms"].items()), flush=True)
