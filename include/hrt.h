@@ -141,7 +141,7 @@ enum {
     HRT_STAGE_MARCH_GEN = 2,      /* segment setup + occupancy DDA sample generation (K4) */
     HRT_STAGE_FIELD = 3,          /* hash encode + tcgen05 MLP field engine (K5/K6) */
     HRT_STAGE_SHADOW = 4,         /* shadow any-hit of NeRF samples (K3) */
-    HRT_STAGE_COMPOSITE = 5,      /* transmittance compositing (K7), dense-grid march */
+    HRT_STAGE_COMPOSITE = 5,      /* transmittance compositing (K7) fused with next-round sample generation, dense-grid march */
     HRT_STAGE_SHADE = 6,          /* BSDF sample, spawn, compaction (K8) */
     HRT_STAGE_ACCUMULATE = 7      /* per-pixel sum / spp (K9) */
 };

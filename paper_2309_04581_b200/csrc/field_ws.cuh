@@ -74,6 +74,20 @@ struct __align__(16) SampleIn {
     int32_t path;
 };
 
+// Logical batch row l -> physical row of the sample-major march batch: the
+// batch of a round is `width` live paths x S samples laid out with row
+// stride `stride` (the previous queue length), i.e. l -> (l / width) *
+// stride + l % width; width == 0 is the identity (dense batches).
+struct RowMap {
+    int64_t stride;
+    int32_t width;
+};
+__device__ __forceinline__ int64_t phys_row(const RowMap& m, int64_t l) {
+    if (m.width == 0) return l;
+    const uint32_t i = (uint32_t)l / (uint32_t)m.width;      // batches stay below 2^31 rows
+    return (int64_t)i * m.stride + (int64_t)((uint32_t)l - i * (uint32_t)m.width);
+}
+
 struct SmemPlan {
     uint32_t w, bars, tslot, total;
 };
@@ -123,9 +137,8 @@ __device__ __forceinline__ void relu64_tmem(uint32_t accum, uint32_t act) {
 // colour head (rgb = 0).
 template <int E, int F>
 __global__ void __launch_bounds__(kThreads, 1)
-k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __restrict__ count,
-           int64_t n_fixed, const float4* __restrict__ dir32, float4* __restrict__ out,
-           int32_t density_only) {
+k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t n,
+           const float4* __restrict__ dir32, float4* __restrict__ out, int32_t density_only) {
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr SmemPlan P = plan(E);
     constexpr nerf::WOff W = nerf::woff(E);
@@ -134,7 +147,6 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __res
     constexpr int NC = NL * F / 2;                // TMEM columns per encode thread
     constexpr uint32_t kStageCols = E / 2;
     const int warp = threadIdx.x >> 5;
-    const int64_t n = count ? (int64_t)*count : n_fixed;
     const int64_t tiles = (n + kRows - 1) / kRows;
 
     // ---- prologue: weights to smem, barriers, TMEM
@@ -174,16 +186,17 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __res
         for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
             const int s = it % kStages;
             const uint32_t ph = (uint32_t)((it / kStages) & 1);
-            const int64_t i = t * kRows + r;
+            const int64_t l = t * kRows + r;
+            const int64_t i = l < n ? phys_row(rmap, l) : 0;
             float v[NL * F];
             if constexpr (kLanePairs) {
                 // lane pair (2p, 2p+1) encodes rows 2p and 2p+1 of the quarter;
                 // lane dx gathers the cx = dx corners of both, then the pair
                 // swaps partial sums so lane 2p keeps row 2p, lane 2p+1 row 2p+1
                 const uint32_t dx = threadIdx.x & 1u;
-                const int64_t iA = i - (int64_t)dx;
-                const SampleIn sa = iA < n ? in[iA] : SampleIn{0.f, 0.f, 0.f, -1};
-                const SampleIn sb = iA + 1 < n ? in[iA + 1] : SampleIn{0.f, 0.f, 0.f, -1};
+                const int64_t lA = l - (int64_t)dx;
+                const SampleIn sa = lA < n ? in[phys_row(rmap, lA)] : SampleIn{0.f, 0.f, 0.f, -1};
+                const SampleIn sb = lA + 1 < n ? in[phys_row(rmap, lA + 1)] : SampleIn{0.f, 0.f, 0.f, -1};
                 const bool va = sa.path >= 0, vb = sb.path >= 0;
                 const float3 ra = make_float3(__fsub_rn(sa.x, lo.x), __fsub_rn(sa.y, lo.y),
                                               __fsub_rn(sa.z, lo.z));
@@ -212,7 +225,7 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __res
                     }
                 }
             } else {
-            const SampleIn si = i < n ? in[i] : SampleIn{0.f, 0.f, 0.f, -1};
+            const SampleIn si = l < n ? in[i] : SampleIn{0.f, 0.f, 0.f, -1};
             if (si.path >= 0) {
                 const float3 rel = make_float3(__fsub_rn(si.x, lo.x), __fsub_rn(si.y, lo.y),
                                                __fsub_rn(si.z, lo.z));
@@ -279,9 +292,10 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, const int32_t* __res
         int it = 0;
         for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
             if ((it % kMlpGroups) != g) continue;
-            const int64_t i = t * kRows + m;
+            const int64_t l = t * kRows + m;
+            const int64_t i = l < n ? phys_row(rmap, l) : 0;
             float3 dir = make_float3(0.f, 0.f, 1.f);
-            const int32_t path = i < n ? in[i].path : -1;
+            const int32_t path = l < n ? in[i].path : -1;
             if (path >= 0 && !density_only) {
                 const float4 d4 = dir32[path];
                 dir = make_float3(d4.x, d4.y, d4.z);

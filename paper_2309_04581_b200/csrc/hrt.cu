@@ -290,33 +290,34 @@ unsigned grid_for(const hrt_handle* h, int64_t n) {
 }
 
 template <int E, int F>
-int launch_ws(hrt_handle* h, const fws::SampleIn* in, const int32_t* count, int64_t n_fixed,
-              int64_t n_max, const float4* dir32, float4* out, int density_only, cudaStream_t st) {
+int launch_ws(hrt_handle* h, const fws::SampleIn* in, fws::RowMap rm, int64_t n, const float4* dir32,
+              float4* out, int density_only, cudaStream_t st) {
     constexpr uint32_t smem = fws::plan(E).total;
     CK(cudaFuncSetAttribute(fws::k_field_ws<E, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int64_t tiles = (n_max + fws::kRows - 1) / fws::kRows;
+    const int64_t tiles = (n + fws::kRows - 1) / fws::kRows;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)h->sm_count));
-    fws::k_field_ws<E, F><<<grid, fws::kThreads, smem, st>>>(h->sc.field.nf, in, count, n_fixed, dir32,
-                                                             out, density_only);
+    fws::k_field_ws<E, F><<<grid, fws::kThreads, smem, st>>>(h->sc.field.nf, in, rm, n, dir32, out,
+                                                             density_only);
     CK(cudaGetLastError());
     return HRT_OK;
 }
 
-// Evaluate a batch (count on the device, at most n_max) with the field engine;
-// bracketed by events so the dominant kernel's device time is measured live.
-int field_ws(hrt_handle* h, const fws::SampleIn* in, const int32_t* count, int64_t n_fixed,
-             int64_t n_max, const float4* dir32, float4* out, int density_only, cudaStream_t st) {
-    if (n_max <= 0) return HRT_OK;
+// Evaluate a batch of n logical rows (RowMap: where they live) with the
+// field engine; bracketed by events so the dominant kernel's device time is
+// measured live.
+int field_ws(hrt_handle* h, const fws::SampleIn* in, fws::RowMap rm, int64_t n, const float4* dir32,
+             float4* out, int density_only, cudaStream_t st) {
+    if (n <= 0) return HRT_OK;
     const bool timed = h->n_timed < kTimedLaunches;
     if (timed) CK(cudaEventRecord(h->mev[2 * h->n_timed], st));
     int rc;
     switch (h->E * 8 + h->F) {
-        case 16 * 8 + 2: rc = launch_ws<16, 2>(h, in, count, n_fixed, n_max, dir32, out, density_only, st); break;
-        case 32 * 8 + 2: rc = launch_ws<32, 2>(h, in, count, n_fixed, n_max, dir32, out, density_only, st); break;
-        case 64 * 8 + 4: rc = launch_ws<64, 4>(h, in, count, n_fixed, n_max, dir32, out, density_only, st); break;
-        case 32 * 8 + 4: rc = launch_ws<32, 4>(h, in, count, n_fixed, n_max, dir32, out, density_only, st); break;
-        case 64 * 8 + 2: rc = launch_ws<64, 2>(h, in, count, n_fixed, n_max, dir32, out, density_only, st); break;
-        case 16 * 8 + 4: rc = launch_ws<16, 4>(h, in, count, n_fixed, n_max, dir32, out, density_only, st); break;
+        case 16 * 8 + 2: rc = launch_ws<16, 2>(h, in, rm, n, dir32, out, density_only, st); break;
+        case 32 * 8 + 2: rc = launch_ws<32, 2>(h, in, rm, n, dir32, out, density_only, st); break;
+        case 64 * 8 + 4: rc = launch_ws<64, 4>(h, in, rm, n, dir32, out, density_only, st); break;
+        case 32 * 8 + 4: rc = launch_ws<32, 4>(h, in, rm, n, dir32, out, density_only, st); break;
+        case 64 * 8 + 2: rc = launch_ws<64, 2>(h, in, rm, n, dir32, out, density_only, st); break;
+        case 16 * 8 + 4: rc = launch_ws<16, 4>(h, in, rm, n, dir32, out, density_only, st); break;
         default: return fail(HRT_EINVAL, "unsupported encoding width");
     }
     if (rc) return rc;
@@ -344,7 +345,7 @@ int field_eval(hrt_handle* h, const double* p, const double* d, int64_t n, float
                                                static_cast<fws::SampleIn*>(in),
                                                static_cast<float4*>(dir), e);
     CK(cudaGetLastError());
-    int rc = field_ws(h, static_cast<fws::SampleIn*>(in), nullptr, n, n, static_cast<float4*>(dir),
+    int rc = field_ws(h, static_cast<fws::SampleIn*>(in), fws::RowMap{0, 0}, n, static_cast<float4*>(dir),
                       static_cast<float4*>(res), density_only, st);
     if (rc == HRT_OK) {
         kern::k_field_post<<<g, kThreads, 0, st>>>(static_cast<float4*>(res), e, n, sigma,
@@ -454,6 +455,15 @@ int read_counter(hrt_handle* h, int idx, cudaStream_t st, int32_t* v) {
     return HRT_OK;
 }
 
+int read_counters2(hrt_handle* h, int i0, int i1, cudaStream_t st, int32_t* v0, int32_t* v1) {
+    CK(cudaMemcpyAsync(h->pinned, h->ps.counters + i0, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h->pinned + 1, h->ps.counters + i1, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *v0 = h->pinned[0];
+    *v1 = h->pinned[1];
+    return HRT_OK;
+}
+
 // ---- stage profiler (hrt_set_profile): pbeg/pend bracket one launch
 constexpr int kProfPairs = 4096;
 
@@ -491,6 +501,42 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
     int rc;
     if ((rc = read_counter(h, C_MQ0, st, &live))) return rc;
     int mc = 0;
+    if (live == 0) return HRT_OK;
+    if (!a.trace) {
+        // fused rounds: k_step (composite previous batch + generate) -> field -> shadow
+        int32_t prev_nq = 0;
+        for (int first = 1;; first = 0) {
+            const int32_t S = (int32_t)std::max<int64_t>(
+                1, std::min<int64_t>(kern::kRoundSamples, h->batch_cap / live));
+            pbeg(h, st);
+            kern::k_round_reset<<<1, 1, 0, st>>>(h->ps.counters, mc ^ 1);
+            kern::k_step<<<grid_for(h, live), kThreads, 0, st>>>(a, h->ms, mc, S, prev_nq, first);
+            CK(cudaGetLastError());
+            pend(h, HRT_STAGE_COMPOSITE, st);
+            h->launches += 2;
+            int32_t nxt = 0, ns = 0;
+            if ((rc = read_counters2(h, C_MQ0 + (mc ^ 1), C_NS, st, &nxt, &ns))) return rc;
+            if (ns == 0) break;
+            // the batch: nxt continuing paths x S rows at stride `live`
+            const fws::RowMap rm{live, nxt};
+            const int64_t rows = (int64_t)nxt * S;
+            pbeg(h, st);
+            if ((rc = field_ws(h, h->ms.in, rm, rows, h->ms.dir32, h->ms.out, 0, st))) return rc;
+            pend(h, HRT_STAGE_FIELD, st);
+            if (h->sc.em.n > 0) {
+                pbeg(h, st);
+                kern::k_shadow<<<grid_for(h, rows), kThreads, 0, st>>>(a, h->ms, rm, rows);
+                CK(cudaGetLastError());
+                pend(h, HRT_STAGE_SHADOW, st);
+                ++h->launches;
+            }
+            ++h->rounds;
+            prev_nq = live;
+            live = nxt;
+            mc ^= 1;
+        }
+        return HRT_OK;
+    }
     while (live > 0) {
         const int32_t S = (int32_t)std::max<int64_t>(
             1, std::min<int64_t>(kern::kRoundSamples, h->batch_cap / live));
@@ -501,14 +547,14 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
         CK(cudaGetLastError());
         pend(h, HRT_STAGE_MARCH_GEN, st);
         pbeg(h, st);
-        if ((rc = field_ws(h, h->ms.in, nullptr, (int64_t)live * S, (int64_t)live * S, h->ms.dir32,
-                           h->ms.out, 0, st)))
+        if ((rc = field_ws(h, h->ms.in, fws::RowMap{0, 0}, (int64_t)live * S, h->ms.dir32, h->ms.out, 0,
+                           st)))
             return rc;
         pend(h, HRT_STAGE_FIELD, st);
         if (h->sc.em.n > 0) {
             const int64_t rows = (int64_t)live * S;
             pbeg(h, st);
-            kern::k_shadow<<<grid_for(h, rows), kThreads, 0, st>>>(a, h->ms, mc, rows);
+            kern::k_shadow<<<grid_for(h, rows), kThreads, 0, st>>>(a, h->ms, fws::RowMap{0, 0}, rows);
             CK(cudaGetLastError());
             pend(h, HRT_STAGE_SHADOW, st);
             ++h->launches;

@@ -326,61 +326,122 @@ __global__ void k_seg(Args a, MarchState m) {
     }
 }
 
+// Generate up to S evaluable midpoints of path p (queue rank j of nq) into
+// the sample-major batch: the i-th sample goes to row i * nq + j, so a warp's
+// lanes are neighbouring paths (adjacent pixels) at the same step -> coherent
+// table gathers. Unused rows of the path become holes (path = -1) that the
+// field engine skips. Returns the count.
+HRT_DEV int32_t gen_path(const Args& a, const MarchState& m, int32_t p, int32_t j, int32_t nq,
+                         int32_t S, const Acc& c) {
+    const PathState& s = a.ps;
+    const DevField& fld = a.sc.field;
+    const NeuralField& nf = fld.nf;
+    int32_t budget = S;
+    if (a.sc.sample_cap > 0) budget = min(budget, a.sc.sample_cap - c.neval);
+    int32_t cnt = 0, k = m.k[p];
+    if (!halted(a.sc, c)) {
+        const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+        Segment g{m.s0[p], m.delta[p], m.n[p]};
+        const d3 of = field_point(fld, o), df = field_dir(fld, d);
+        while (cnt < budget && k < g.n) {
+            const d3 xf = field_point(fld, sample_point(o, d, g, k));
+            if (!inside_box(fld.lo, fld.hi, xf)) { ++k; continue; }
+            int32_t cell3[3];
+            const int32_t cell = nerf::occ_cell(nf, xf, cell3);
+            if (nerf::occ_test(nf, cell)) {
+                const float3 p32 = nerf::to_f32(xf);
+                fws::SampleIn r;
+                r.x = p32.x; r.y = p32.y; r.z = p32.z; r.path = p;
+                m.in[(int64_t)cnt * nq + j] = r;
+                m.sk[(int64_t)cnt * nq + j] = k;
+                ++cnt;
+                ++k;
+            } else {
+                k = dda_next(nf, fld, of, df, g, k, cell3);
+            }
+        }
+    }
+    for (int32_t i = cnt; i < S; ++i) {
+        fws::SampleIn r;
+        r.x = r.y = r.z = 0.f;
+        r.path = -1;
+        m.in[(int64_t)i * nq + j] = r;
+    }
+    m.cnt[p] = cnt;
+    m.k[p] = k;
+    return cnt;
+}
+
+// Composite the cnt samples path p left at rows i * nq + j (field.py:244-255
+// per sample, in k order, fp64) with their shadow masks, the sample cap and
+// the early-out. Returns true if the path halted inside the batch.
+#ifndef HRT_COMP_BATCH
+#define HRT_COMP_BATCH 4
+#endif
+constexpr int32_t kCompBatch = HRT_COMP_BATCH;
+
+template <bool kTrace>
+HRT_DEV bool comp_path(const Args& a, const MarchState& m, int32_t p, int32_t j, int32_t nq,
+                       int32_t cnt, double delta, Acc& c, int32_t& done) {
+    bool stop = false;
+    // rows are read kCompBatch at a time ahead of the (sequential) halt
+    // test, so a path waits one memory latency per batch, not per sample
+    for (int32_t i0 = 0; i0 < cnt && !stop; i0 += kCompBatch) {
+        float4 fb[kCompBatch];
+        int32_t cb[kCompBatch];
+#pragma unroll
+        for (int32_t u = 0; u < kCompBatch; ++u) {
+            const int64_t row = (int64_t)(i0 + u) * nq + j;
+            const bool in = i0 + u < cnt;
+            fb[u] = in ? __ldcs(&m.out[row]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            cb[u] = (in && a.sc.em.n > 0) ? __ldcs(&m.shadow[row]) : 0;
+        }
+#pragma unroll
+        for (int32_t u = 0; u < kCompBatch; ++u) {
+            const int32_t i = i0 + u;
+            if (i >= cnt) break;
+            if (halted(a.sc, c)) { stop = true; break; }
+            const float4 f = fb[u];
+            const double rgb[3] = {(double)f.y, (double)f.z, (double)f.w};
+            const double al = 1.0 - exp(-(double)f.x * delta);
+            const double mask = path::mask_of(a.sc, cb[u]);
+            c.neval += 1;
+            ++done;
+            composite_m(c, al, rgb, mask);
+            if (kTrace) {
+                const int64_t row = (int64_t)i * nq + j;
+                const int32_t k = m.sk[row];
+                const fws::SampleIn r = m.in[row];
+                int32_t c3[3];
+                const int32_t cell = nerf::occ_cell(a.sc.field.nf, mk(r.x, r.y, r.z), c3);
+                const int64_t slot = atomicAdd(&a.ps.counters[C_TRACE], 1);
+                if (slot < a.trace_cap)
+                    reinterpret_cast<int4*>(a.trace)[slot] = make_int4(p, a.bounce, k, cell);
+            }
+        }
+    }
+    return stop;
+}
+
+HRT_DEV void warp_stat_add(unsigned long long* stats, int which, int32_t v) {
+    const int32_t t = __reduce_add_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && t) stat_add(stats, which, t);
+}
+
+// Unfused round (used with the debug trace): k_gen -> field -> k_comp.
 __global__ void k_gen(Args a, MarchState m, int32_t mcur, int32_t S) {
     const int32_t nq = a.ps.counters[C_MQ0 + mcur];
     const int32_t* q = pick(m.mq, mcur);
     const PathState& s = a.ps;
-    const DevField& fld = a.sc.field;
-    const NeuralField& nf = fld.nf;
     for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += gridDim.x * blockDim.x) {
         const int32_t p = q[j];
         Acc c;
         c.Ts[0] = s.Tr[p]; c.Ts[1] = s.Tg[p]; c.Ts[2] = s.Tb[p];
         c.neval = s.neval[p];
-        int32_t budget = S;
-        if (a.sc.sample_cap > 0) budget = min(budget, a.sc.sample_cap - c.neval);
-        int32_t cnt = 0, k = m.k[p];
-        // sample-major batch: the i-th sample of the path with queue rank j
-        // goes to row i * nq + j, so a warp's lanes are neighbouring paths
-        // (adjacent pixels) at the same step -> coherent table gathers
-        if (!halted(a.sc, c)) {
-            const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
-            Segment g{m.s0[p], m.delta[p], m.n[p]};
-            const d3 of = field_point(fld, o), df = field_dir(fld, d);
-            while (cnt < budget && k < g.n) {
-                const d3 xf = field_point(fld, sample_point(o, d, g, k));
-                if (!inside_box(fld.lo, fld.hi, xf)) { ++k; continue; }
-                int32_t cell3[3];
-                const int32_t cell = nerf::occ_cell(nf, xf, cell3);
-                if (nerf::occ_test(nf, cell)) {
-                    const float3 p32 = nerf::to_f32(xf);
-                    fws::SampleIn r;
-                    r.x = p32.x; r.y = p32.y; r.z = p32.z; r.path = p;
-                    m.in[(int64_t)cnt * nq + j] = r;
-                    m.sk[(int64_t)cnt * nq + j] = k;
-                    ++cnt;
-                    ++k;
-                } else {
-                    k = dda_next(nf, fld, of, df, g, k, cell3);
-                }
-            }
-        }
-        for (int32_t i = cnt; i < S; ++i) {          // holes: skipped by the field engine
-            fws::SampleIn r;
-            r.x = r.y = r.z = 0.f;
-            r.path = -1;
-            m.in[(int64_t)i * nq + j] = r;
-        }
+        const int32_t cnt = gen_path(a, m, p, j, nq, S, c);
         if (cnt) atomicAdd(&a.ps.counters[C_NS], cnt);
-        m.cnt[p] = cnt;
-        m.k[p] = k;
     }
 }
-
-#ifndef HRT_COMP_BATCH
-#define HRT_COMP_BATCH 4
-#endif
-constexpr int32_t kCompBatch = HRT_COMP_BATCH;
 
 #ifndef HRT_COMP_MINB
 #define HRT_COMP_MINB 1
@@ -392,69 +453,69 @@ __global__ void __launch_bounds__(256, HRT_COMP_MINB) k_comp(Args a, MarchState 
     int32_t* next = pick(m.mq, mcur ^ 1);
     int32_t* next_n = &a.ps.counters[C_MQ0 + (mcur ^ 1)];
     const PathState& s = a.ps;
-    const NeuralField& nf = a.sc.field.nf;
     int32_t done = 0;
     for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += gridDim.x * blockDim.x) {
         const int32_t p = q[j];
         Acc c;
         load_acc(s, p, c);
-        const int32_t cnt = m.cnt[p];
-        const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
-        const Segment g{m.s0[p], m.delta[p], m.n[p]};
-        bool stop = false;
-        // rows are read kCompBatch at a time ahead of the (sequential) halt
-        // test, so a path waits one memory latency per batch, not per sample
-        for (int32_t i0 = 0; i0 < cnt && !stop; i0 += kCompBatch) {
-            float4 fb[kCompBatch];
-            int32_t cb[kCompBatch];
-#pragma unroll
-            for (int32_t u = 0; u < kCompBatch; ++u) {
-                const int64_t row = (int64_t)(i0 + u) * nq + j;
-                const bool in = i0 + u < cnt;
-                fb[u] = in ? __ldcs(&m.out[row]) : make_float4(0.f, 0.f, 0.f, 0.f);
-                cb[u] = (in && a.sc.em.n > 0) ? __ldcs(&m.shadow[row]) : 0;
-            }
-#pragma unroll
-            for (int32_t u = 0; u < kCompBatch; ++u) {
-            const int32_t i = i0 + u;
-            if (i >= cnt) break;
-            if (halted(a.sc, c)) { stop = true; break; }
-            const int64_t row = (int64_t)i * nq + j;
-            const float4 f = fb[u];
-            const double rgb[3] = {(double)f.y, (double)f.z, (double)f.w};
-            const double al = 1.0 - exp(-(double)f.x * g.delta);
-            const double mask = path::mask_of(a.sc, cb[u]);
-            c.neval += 1;
-            ++done;
-            composite_m(c, al, rgb, mask);
-            if (kTrace) {
-                const int32_t k = m.sk[row];
-                const fws::SampleIn r = m.in[row];
-                int32_t c3[3];
-                const int32_t cell = nerf::occ_cell(nf, mk(r.x, r.y, r.z), c3);
-                const int64_t slot = atomicAdd(&a.ps.counters[C_TRACE], 1);
-                if (slot < a.trace_cap)
-                    reinterpret_cast<int4*>(a.trace)[slot] = make_int4(p, a.bounce, k, cell);
-            }
-            }
-        }
+        const bool stop = comp_path<kTrace>(a, m, p, j, nq, m.cnt[p], m.delta[p], c, done);
         store_acc(s, p, c);
-        if (!stop && !halted(a.sc, c) && m.k[p] < g.n) next[reserve(next_n)] = p;
+        if (!stop && !halted(a.sc, c) && m.k[p] < m.n[p]) next[reserve(next_n)] = p;
     }
     if (done) stat_add(a.ps.stats, S_SAMPLES, done);
     if (blockIdx.x == 0 && threadIdx.x == 0) stat_add(a.ps.stats, S_EVALS, a.ps.counters[C_NS]);
+}
+
+// Fused round: every path of queue mcur first composites the samples it left
+// in the previous batch (rows i * prev_nq + base[p]; none on the first
+// round), then - if it goes on - takes rank r in the other queue and
+// generates its next samples at rows i * nq + r. One pass over the path
+// state per round instead of two (k_gen + k_comp); a path whose remaining
+// candidates are all empty cells keeps a rank with S hole rows.
+__global__ void __launch_bounds__(256, 1) k_step(Args a, MarchState m, int32_t mcur, int32_t S,
+                                               int32_t prev_nq, int32_t first) {
+    const int32_t nq = a.ps.counters[C_MQ0 + mcur];
+    const int32_t* q = pick(m.mq, mcur);
+    int32_t* next = pick(m.mq, mcur ^ 1);
+    int32_t* next_n = &a.ps.counters[C_MQ0 + (mcur ^ 1)];
+    const PathState& s = a.ps;
+    int32_t done = 0, made = 0;
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += gridDim.x * blockDim.x) {
+        const int32_t p = q[j];
+        Acc c;
+        load_acc(s, p, c);
+        bool go = true;
+        if (!first) {
+            const bool stop = comp_path<false>(a, m, p, m.base[p], prev_nq, m.cnt[p], m.delta[p], c,
+                                               done);
+            store_acc(s, p, c);
+            go = !stop && !halted(a.sc, c) && m.k[p] < m.n[p];
+        }
+        if (go) {
+            // dense next batch: rank r among the paths that go on; rows
+            // i * nq + r (the field engine reads them through a RowMap)
+            const int32_t r = reserve(next_n);
+            next[r] = p;
+            m.base[p] = r;
+            made += gen_path(a, m, p, r, nq, S, c);
+        }
+    }
+    warp_stat_add(a.ps.stats, S_SAMPLES, done);
+    warp_stat_add(a.ps.stats, S_EVALS, made);
+    const int32_t any = __reduce_add_sync(0xffffffffu, made);
+    if ((threadIdx.x & 31) == 0 && any) atomicAdd(&a.ps.counters[C_NS], any);
 }
 
 // K3 over the batch: one thread per sample row (sample-major, so a warp
 // traces the shadow rays of 32 neighbouring pixels at the same step). Rows
 // that cannot contribute (opacity 0 or black) cast no ray, as in the
 // reference (field.py:246-251).
-__global__ void k_shadow(Args a, MarchState m, int32_t mcur, int64_t rows) {
-    const int32_t nq = a.ps.counters[C_MQ0 + mcur];
+__global__ void k_shadow(Args a, MarchState m, fws::RowMap rm, int64_t rows) {
     const PathState& s = a.ps;
     int32_t cast = 0;
-    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < rows;
-         row += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < rows;
+         l += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = fws::phys_row(rm, l);
         const int32_t p = m.in[row].path;
         if (p < 0) continue;
         const float4 f = m.out[row];
@@ -472,7 +533,6 @@ __global__ void k_shadow(Args a, MarchState m, int32_t mcur, int64_t rows) {
         }
         m.shadow[row] = code;
     }
-    (void)nq;
     if (cast) stat_add(a.ps.stats, S_SHADOW, cast);
 }
 
