@@ -141,6 +141,195 @@ HRT_DEV bool any_hit(const DevBvh& b, d3 o, d3 d, double t_min, double t_max) {
     return false;
 }
 
+// ------------------------------------------- float32-culled traversal
+// Box tests run in float32 on WNode (half the bytes of the float64 tree,
+// both children per 64-byte load); they only cull, never decide: the boxes
+// are rounded outward and padded by 1e-5 * max(1, |coord|), the ray
+// interval is widened by 1e-5 relative + absolute, so every box the exact
+// test would enter is entered here, and every candidate triangle goes
+// through the float64 Moller-Trumbore above. Hits are therefore the
+// reference's (nearest t, ties to the smaller face id) bit for bit.
+struct Ray32 {
+    float ox, oy, oz, ix, iy, iz;
+};
+
+HRT_DEV Ray32 prep32(d3 o, d3 d) {
+    Ray32 r;
+    r.ox = (float)o.x; r.oy = (float)o.y; r.oz = (float)o.z;
+    r.ix = 1.0f / (float)d.x; r.iy = 1.0f / (float)d.y; r.iz = 1.0f / (float)d.z;
+    return r;
+}
+
+HRT_DEV float t_lo32(double t) { return t <= 0.0 ? (float)t * 1.00001f - 1e-5f : (float)t * 0.99999f - 1e-5f; }
+HRT_DEV float t_hi32(double t) { return (float)t * 1.00001f + 1e-5f; }
+
+// NaN (0 * inf: axis-aligned ray on a slab plane) widens to the whole axis.
+HRT_DEV void slab_axis(float lo, float hi, float o, float inv, float& tn, float& tf) {
+    const float ta = (lo - o) * inv, tb = (hi - o) * inv;
+    const bool nan = (ta != ta) || (tb != tb);
+    tn = fmaxf(tn, nan ? -INFINITY : fminf(ta, tb));
+    tf = fminf(tf, nan ? INFINITY : fmaxf(ta, tb));
+}
+
+HRT_DEV bool box32(float lx, float ly, float lz, float hx, float hy, float hz, const Ray32& r,
+                   float t0, float t1, float& near) {
+    float tn = t0, tf = t1;
+    slab_axis(lx, hx, r.ox, r.ix, tn, tf);
+    slab_axis(ly, hy, r.oy, r.iy, tn, tf);
+    slab_axis(lz, hz, r.oz, r.iz, tn, tf);
+    near = tn;
+    return tn <= tf;
+}
+
+HRT_DEV void wchildren(const WNode& w, const Ray32& r, float t0, float t1, bool& h0, bool& h1,
+                       float& n0, float& n1) {
+    h0 = box32(w.a.x, w.a.y, w.a.z, w.a.w, w.b.x, w.b.y, r, t0, t1, n0);
+    h1 = box32(w.b.z, w.b.w, w.c.x, w.c.y, w.c.z, w.c.w, r, t0, t1, n1);
+}
+
+HRT_DEV WNode load_w(const WNode* __restrict__ nodes, int32_t i) {
+    const float4* p = reinterpret_cast<const float4*>(nodes + i);
+    WNode w;
+    w.a = __ldg(p);
+    w.b = __ldg(p + 1);
+    w.c = __ldg(p + 2);
+    w.r = __ldg(reinterpret_cast<const int4*>(p + 3));
+    return w;
+}
+
+// Leaf of ref (< 0): nearest-hit update over its triangles.
+HRT_DEV void leaf_closest(const DevBvh& b, int32_t ref, d3 o, d3 d, double t_min, double t_max,
+                          double& best_t, int32_t& best_f) {
+    const int32_t code = ~ref, first = code >> 3, count = code & 7;
+    for (int i = 0; i < count; ++i) {
+        const int32_t li = first + i;
+        const double t = moller_trumbore(o, d, b.tri + 9 * (size_t)li, t_min, t_max);
+        if (t < INFINITY) {
+            const int32_t f = b.tri_id[li];
+            if (t < best_t || (t == best_t && f < best_f)) { best_t = t; best_f = f; }
+        }
+    }
+}
+
+HRT_DEV bool leaf_any(const DevBvh& b, int32_t ref, d3 o, d3 d, double t_min, double t_max) {
+    const int32_t code = ~ref, first = code >> 3, count = code & 7;
+    for (int i = 0; i < count; ++i)
+        if (moller_trumbore(o, d, b.tri + 9 * (size_t)(first + i), t_min, t_max) < INFINITY) return true;
+    return false;
+}
+
+// Nearest hit (surface.py:377-440 contract); global face id or -1.
+HRT_DEV int32_t closest_w(const DevBvh& b, d3 o, d3 d, double t_min, double t_max, double& best_t) {
+    best_t = INFINITY;
+    int32_t best_f = -1;
+    if (b.n_faces == 0) return -1;
+    const Ray32 r = prep32(o, d);
+    const float t0 = t_lo32(t_min);
+    int32_t stack[kStack];
+    float stack_t[kStack];
+    int sp = 0;
+    int32_t cur = 0;
+    while (true) {
+        const WNode w = load_w(b.wnodes, cur);
+        const float t1 = t_hi32(fmin(t_max, best_t));
+        bool h0, h1;
+        float n0, n1;
+        wchildren(w, r, t0, t1, h0, h1, n0, n1);
+        if (h0 && w.r.x < 0) { leaf_closest(b, w.r.x, o, d, t_min, t_max, best_t, best_f); h0 = false; }
+        if (h1 && w.r.y < 0) { leaf_closest(b, w.r.y, o, d, t_min, t_max, best_t, best_f); h1 = false; }
+        if (h0 && h1) {
+            const bool first0 = n0 <= n1;
+            if (sp < kStack) {
+                stack[sp] = first0 ? w.r.y : w.r.x;
+                stack_t[sp] = first0 ? n1 : n0;
+                ++sp;
+            }
+            cur = first0 ? w.r.x : w.r.y;
+            continue;
+        }
+        if (h0 || h1) { cur = h0 ? w.r.x : w.r.y; continue; }
+        // pop, skipping subtrees whose entry lies beyond the current best hit
+        bool found = false;
+        const float lim = t_hi32(fmin(t_max, best_t));
+        while (sp > 0) {
+            --sp;
+            if (stack_t[sp] <= lim) { cur = stack[sp]; found = true; break; }
+        }
+        if (!found) break;
+    }
+    return best_f;
+}
+
+// True if any face lies in (t_min, t_max] (surface.py:442-478).
+HRT_DEV bool any_hit_w(const DevBvh& b, d3 o, d3 d, double t_min, double t_max) {
+    if (b.n_faces == 0) return false;
+    const Ray32 r = prep32(o, d);
+    const float t0 = t_lo32(t_min), t1 = t_hi32(t_max);
+    int32_t stack[kStack];
+    int sp = 0;
+    int32_t cur = 0;
+    while (true) {
+        const WNode w = load_w(b.wnodes, cur);
+        bool h0, h1;
+        float n0, n1;
+        wchildren(w, r, t0, t1, h0, h1, n0, n1);
+        if (h0 && w.r.x < 0) {
+            if (leaf_any(b, w.r.x, o, d, t_min, t_max)) return true;
+            h0 = false;
+        }
+        if (h1 && w.r.y < 0) {
+            if (leaf_any(b, w.r.y, o, d, t_min, t_max)) return true;
+            h1 = false;
+        }
+        if (h0 && h1) {
+            if (sp < kStack) stack[sp++] = w.r.y;
+            cur = w.r.x;
+            continue;
+        }
+        if (h0 || h1) { cur = h0 ? w.r.x : w.r.y; continue; }
+        if (sp == 0) break;
+        cur = stack[--sp];
+    }
+    return false;
+}
+
+#ifndef HRT_BVH64
+#define HRT_BVH64 0      // 1: traverse the float64 tree (reference-order culling)
+#endif
+HRT_DEV int32_t nearest(const DevBvh& b, d3 o, d3 d, double t_min, double t_max, double& best_t) {
+    return HRT_BVH64 ? closest(b, o, d, t_min, t_max, best_t) : closest_w(b, o, d, t_min, t_max, best_t);
+}
+HRT_DEV bool occluded(const DevBvh& b, d3 o, d3 d, double t_min, double t_max) {
+    return HRT_BVH64 ? any_hit(b, o, d, t_min, t_max) : any_hit_w(b, o, d, t_min, t_max);
+}
+
+// WNode child boxes from the float64 tree after a refit (src: float64 node
+// index per child slot, -1 = empty). Same rounding as the host (hrt.cu wbox).
+HRT_DEV void wbox_dev(const BvhNode& n, float lo[3], float hi[3]) {
+    double mag = 1.0;
+    for (int a = 0; a < 3; ++a) mag = fmax(mag, fmax(fabs(n.lo[a]), fabs(n.hi[a])));
+    const double pad = 1e-5 * mag;
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = __double2float_rd(n.lo[a] - pad);
+        hi[a] = __double2float_ru(n.hi[a] + pad);
+    }
+}
+
+__global__ void k_wsync(WNode* w, const int2* __restrict__ src, const BvhNode* __restrict__ nodes,
+                        int32_t n) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int2 sidx = src[i];
+        float l0[3], h0[3], l1[3], h1[3];
+        if (sidx.x >= 0) wbox_dev(nodes[sidx.x], l0, h0);
+        else { l0[0] = l0[1] = l0[2] = h0[0] = h0[1] = h0[2] = 1e30f; }
+        if (sidx.y >= 0) wbox_dev(nodes[sidx.y], l1, h1);
+        else { l1[0] = l1[1] = l1[2] = h1[0] = h1[1] = h1[2] = 1e30f; }
+        w[i].a = make_float4(l0[0], l0[1], l0[2], h0[0]);
+        w[i].b = make_float4(h0[1], h0[2], l1[0], l1[1]);
+        w[i].c = make_float4(l1[2], h1[0], h1[1], h1[2]);
+    }
+}
+
 // ------------------------------------------------------------ GPU refit (K11)
 // Moving meshes keep their topology; the tree is refit bottom-up: each leaf
 // rebuilds its padded box from its (new) triangles, then climbs; at every

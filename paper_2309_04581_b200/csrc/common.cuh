@@ -61,7 +61,18 @@ struct BvhNode {            // 56 B, float64 bounds (conservatively padded)
     int32_t count;          // > 0 leaf
 };
 
+// Traversal node: both children's boxes inline in float32, rounded outward
+// and padded (see hrt.cu wbox), so one 64-byte load decides both children.
+// ref >= 0: inner node index; ref < 0: leaf ~((first << 3) | count).
+struct __align__(16) WNode {
+    float4 a;   // lo0.x lo0.y lo0.z hi0.x
+    float4 b;   // hi0.y hi0.z lo1.x lo1.y
+    float4 c;   // lo1.z hi1.x hi1.y hi1.z
+    int4 r;     // ref0, ref1, -, -
+};
+
 struct DevBvh {
+    const WNode* wnodes;    // float32-culling traversal tree (same leaves)
     const BvhNode* nodes;
     const double* tri;      // leaf-ordered: v0, e1, e2 (9 doubles)
     const int32_t* tri_id;  // leaf order -> global face id

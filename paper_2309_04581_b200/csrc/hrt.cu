@@ -46,6 +46,8 @@ constexpr bool kTiledFrame = HRT_TILED_FRAME;      // full frames walk 16x16 pix
 }  // namespace
 
 struct RefitState {              // device side of a BVH's GPU refit
+    int2* wsrc = nullptr;        // float64 node behind each WNode child slot
+    int32_t n_w = 0;
     int32_t* parent = nullptr;
     int32_t* leaves = nullptr;
     int32_t* visits = nullptr;
@@ -156,13 +158,91 @@ int refit_gpu(hrt_handle* h, const hrt::BvhHost& b, RefitState& r, DevBvh& dev, 
     bvh::k_refit<<<g2, 256>>>(const_cast<BvhNode*>(dev.nodes), r.parent, r.leaves, r.n_leaves, dev.tri,
                               r.visits);
     CK(cudaGetLastError());
+    const unsigned g3 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((r.n_w + 255) / 256, 148 * 16));
+    bvh::k_wsync<<<g3, 256>>>(const_cast<WNode*>(dev.wnodes), r.wsrc, dev.nodes, r.n_w);
+    CK(cudaGetLastError());
     return HRT_OK;
 }
 
-int upload_bvh(hrt_handle* h, const hrt::BvhHost& b, DevBvh& out) {
+// float64 -> float32 rounded toward -inf / +inf (device: __double2float_rd/ru)
+float f_rd(double x) {
+    float f = (float)x;
+    if ((double)f > x) f = std::nextafter(f, -INFINITY);
+    return f;
+}
+float f_ru(double x) {
+    float f = (float)x;
+    if ((double)f < x) f = std::nextafter(f, INFINITY);
+    return f;
+}
+
+// Child box of a WNode: the float64 node box padded by 1e-5 * max(1, |coord|)
+// and rounded outward (same rule as bvh.cuh wbox_dev, used after refits).
+void wbox(const hrt::BvhNodeHost& n, float lo[3], float hi[3]) {
+    double mag = 1.0;
+    for (int a = 0; a < 3; ++a) mag = std::max(mag, std::max(std::fabs(n.lo[a]), std::fabs(n.hi[a])));
+    const double pad = 1e-5 * mag;
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = f_rd(n.lo[a] - pad);
+        hi[a] = f_ru(n.hi[a] + pad);
+    }
+}
+
+// float32-culling tree over the same leaves: one WNode per inner float64
+// node (a root leaf gets a WNode with an empty second child); src records
+// the float64 node behind each child slot for k_wsync after refits.
+void build_wnodes(const hrt::BvhHost& b, std::vector<WNode>& w, std::vector<int2>& src) {
+    const auto& nd = b.nodes;
+    std::vector<int32_t> widx(nd.size(), -1);
+    int32_t nw = 0;
+    for (size_t i = 0; i < nd.size(); ++i)
+        if (nd[i].count == 0) widx[i] = nw++;
+    auto ref = [&](int32_t c) -> int32_t {
+        return nd[c].count > 0 ? ~((nd[c].first << 3) | nd[c].count) : widx[c];
+    };
+    auto fill = [&](WNode& x, int32_t c0, int32_t c1) {
+        float l0[3], h0[3], l1[3], h1[3];
+        for (int a = 0; a < 3; ++a) l0[a] = h0[a] = l1[a] = h1[a] = 1e30f;
+        if (c0 >= 0) wbox(nd[c0], l0, h0);
+        if (c1 >= 0) wbox(nd[c1], l1, h1);
+        x.a = make_float4(l0[0], l0[1], l0[2], h0[0]);
+        x.b = make_float4(h0[1], h0[2], l1[0], l1[1]);
+        x.c = make_float4(l1[2], h1[0], h1[1], h1[2]);
+        x.r = make_int4(c0 >= 0 ? ref(c0) : -1, c1 >= 0 ? ref(c1) : -1, 0, 0);
+    };
+    if (nd[0].count > 0) {           // whole mesh in one leaf
+        w.assign(1, WNode{});
+        src.assign(1, make_int2(0, -1));
+        fill(w[0], 0, -1);
+        return;
+    }
+    w.assign(nw, WNode{});
+    src.assign(nw, make_int2(-1, -1));
+    for (size_t i = 0; i < nd.size(); ++i) {
+        if (nd[i].count != 0) continue;
+        const int32_t c = nd[i].first;
+        fill(w[widx[i]], c, c + 1);
+        src[widx[i]] = make_int2(c, c + 1);
+    }
+}
+
+int upload_bvh(hrt_handle* h, const hrt::BvhHost& b, DevBvh& out, int2** wsrc, int32_t* n_w) {
     out.n_faces = b.n_faces;
-    out.nodes = nullptr; out.tri = nullptr; out.tri_id = nullptr;
+    out.nodes = nullptr; out.tri = nullptr; out.tri_id = nullptr; out.wnodes = nullptr;
+    *wsrc = nullptr;
+    *n_w = 0;
     if (b.n_faces == 0) return HRT_OK;
+    {
+        std::vector<WNode> w;
+        std::vector<int2> src;
+        build_wnodes(b, w, src);
+        WNode* dw;
+        int rc;
+        if ((rc = h->upload(w.data(), w.size(), &dw))) return rc;
+        if ((rc = h->upload(src.data(), src.size(), wsrc))) return rc;
+        out.wnodes = dw;
+        *n_w = (int32_t)w.size();
+    }
     static_assert(sizeof(BvhNode) == sizeof(hrt::BvhNodeHost), "node layout");
     BvhNode* nodes;
     double* tri;
@@ -662,8 +742,8 @@ int hrt_create(const hrt_scene_desc* d, hrt_handle** out) {
     int rc;
     h->bvh = hrt::build_bvh(d->n_faces, d->v0, d->e1, d->e2);
     h->blk = hrt::build_bvh(d->n_blockers, d->bv0, d->be1, d->be2);
-    if ((rc = upload_bvh(h, h->bvh, sc.bvh))) return bail(rc);
-    if ((rc = upload_bvh(h, h->blk, sc.blockers))) return bail(rc);
+    if ((rc = upload_bvh(h, h->bvh, sc.bvh, &h->rf.wsrc, &h->rf.n_w))) return bail(rc);
+    if ((rc = upload_bvh(h, h->blk, sc.blockers, &h->rfb.wsrc, &h->rfb.n_w))) return bail(rc);
     if ((rc = setup_refit(h, h->bvh, h->rf))) return bail(rc);
     if ((rc = setup_refit(h, h->blk, h->rfb))) return bail(rc);
     double *normal, *emission;

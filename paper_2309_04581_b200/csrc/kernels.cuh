@@ -134,7 +134,7 @@ __global__ void k_intersect(Args a) {
         double t = INFINITY;
         int32_t f = -1;
         if (!a.volume)
-            f = bvh::closest(a.sc.bvh, mk(s.ox[p], s.oy[p], s.oz[p]), mk(s.dx[p], s.dy[p], s.dz[p]),
+            f = bvh::nearest(a.sc.bvh, mk(s.ox[p], s.oy[p], s.oz[p]), mk(s.dx[p], s.dy[p], s.dz[p]),
                              0.0, INFINITY, t);
         s.t_hit[p] = t;
         s.face[p] = f;
@@ -737,10 +737,10 @@ __global__ void k_rays(DevBvh b, const double* o, const double* d, const double*
         const d3 dd = mk(d[3 * i], d[3 * i + 1], d[3 * i + 2]);
         const double t0 = tmin ? tmin[i] : 0.0, t1 = tmax ? tmax[i] : INFINITY;
         if (any) {
-            hit_out[i] = bvh::any_hit(b, oo, dd, t0, t1) ? 1 : 0;
+            hit_out[i] = bvh::occluded(b, oo, dd, t0, t1) ? 1 : 0;
         } else {
             double t;
-            const int32_t f = bvh::closest(b, oo, dd, t0, t1, t);
+            const int32_t f = bvh::nearest(b, oo, dd, t0, t1, t);
             t_out[i] = t;
             f_out[i] = f;
         }

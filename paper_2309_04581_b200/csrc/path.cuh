@@ -115,7 +115,7 @@ HRT_DEV int32_t shadow_code(const DevScene& sc, d3 p, uint64_t seed, int64_t pix
     const double dist = norm(delta);
     const double safe = fmax(dist, 1e-12);
     const d3 dir = {delta.x / safe, delta.y / safe, delta.z / safe};
-    const bool blocked = bvh::any_hit(sc.blockers, p, dir, sc.spawn_eps, dist * (1.0 - 1e-4));
+    const bool blocked = bvh::occluded(sc.blockers, p, dir, sc.spawn_eps, dist * (1.0 - 1e-4));
     return blocked ? idx + 1 : 0;
 }
 
