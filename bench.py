@@ -119,8 +119,9 @@ def peaks():
 
 
 def ncu_traffic():
-    """dram bytes per march launch from the committed ncu --set full summary."""
-    path = os.path.join(ROOT, "profiles", "march_traffic.json")
+    """Per-launch DRAM bytes and L2->L1 sectors per sample of the field engine
+    from the committed ncu capture (profiles/r01_field_traffic.json)."""
+    path = os.path.join(ROOT, "profiles", "r01_field_traffic.json")
     try:
         with open(path) as f:
             return json.load(f)
@@ -328,13 +329,24 @@ def run_ours(args, rank, world, local):
         dist.all_reduce(e2max, op=dist.ReduceOp.MAX)
     e2e_value = float(e2[1]) / (float(e2max[0]) * 1e-3)
 
+    # ---- untimed extras: per-stage breakdown of one frame, gather roofline probe
+    r.set_profile(True)
+    r.render_pixels(cams[0], 1, 0, pixels=pix, out=out[:n_local])
+    stages = {k: round(v, 3) for k, v in r.last_stats["stage_ms"].items()}
+    stage_frame_ms = r.last_stats["ms"]
+    r.set_profile(False)
+    gather_gbs = r.gather_peak(2)
+
     if rank == 0:
         hbm, tflops, peak_src = peaks()
         enc_bytes = 8 * field.n_levels * field.n_features * 4            # 1024 B / sample
         mlp_flop = 2 * (field.enc_dim * 64 + 64 * 16 + 31 * 64 + 64 * 64 + 64 * 3)
         march_samples = evaluated                                          # rank-0 field-engine evaluations
         achieved = march_samples * enc_bytes / (march_ms * 1e-3) / 1e9
-        traffic = ncu_traffic()
+        traffic = ncu_traffic() or {}
+        field_sps = march_samples / (march_ms * 1e-3)                      # samples/s inside the engine
+        sec_per_sample = traffic.get("l2_sectors_per_sample")
+        peak_sectors = gather_gbs * 1e9 / 8.0                              # one sector per random gather
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
@@ -351,10 +363,21 @@ def run_ours(args, rank, world, local):
             "roofline": {
                 "bound": "hbm", "kernel": "fws::k_field_ws<32,2> (warp-specialized hash encode + 5-layer tcgen05 MLP, TMEM operands)",
                 "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                "traffic": traffic.get("dram_bytes_per_launch"),
                 "bytes_per_sample": enc_bytes, "launches": int(march_n),
                 "avg_launch_ms": march_ms / max(1, march_n),
-                "peak_source": peak_src + " hbm_gbs (burst copy); the 46.5 MiB table is L2-resident",
+                "peak_source": peak_src + " hbm_gbs (burst copy); the 46.5 MiB table is L2-resident, "
+                               "so frac > 1 vs HBM: the real limiter is roofline_gather",
+            },
+            "roofline_gather": {
+                "bound": "l2->l1 random-sector gathers (L1 miss path, ~1 sector/clk/SM)",
+                "achieved": field_sps * sec_per_sample if sec_per_sample else None,
+                "peak": peak_sectors, "unit": "sectors/s",
+                "frac": field_sps * sec_per_sample / peak_sectors if sec_per_sample else None,
+                "sectors_per_sample": sec_per_sample,
+                "peak_source": "hrt_gather_peak (live, this run): independent random 8-B gathers over the "
+                               f"same table, {gather_gbs:.0f} GB/s useful; sectors/sample from "
+                               "profiles/r01_field_traffic.json (ncu lts__t_sectors_srcunit_tex_op_read)",
             },
             "roofline_mlp": {"bound": "tensor", "achieved": march_samples * mlp_flop / (march_ms * 1e-3) / 1e12,
                              "peak": tflops, "unit": "TFLOP/s",
@@ -364,6 +387,8 @@ def run_ours(args, rank, world, local):
                     "h2d_bytes_per_step": int(4 * n_local), "d2h_bytes_per_step": int(24 * n_local),
                     "path": "hrt_render_host (host pixel list in, host float64 frame out), wall clock"},
             "clocks": clk,
+            "stages_ms": {"frame_ms": stage_frame_ms, **stages,
+                          "note": "one untimed camera-0 frame with hrt_set_profile (event pair per launch)"},
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_block(args.cpu_tiles)

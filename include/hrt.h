@@ -178,6 +178,11 @@ int hrt_set_trace(hrt_handle* h, int32_t* records, int64_t cap);
  * (on != 0) or off (default). Measurement aid: adds one event pair per launch. */
 int hrt_set_profile(hrt_handle* h, int32_t on);
 
+/* Roofline probe of the hash-grid encode: useful GB/s (8 B per gather) of
+ * independent random 8-byte gathers over this scene's hash table (F = 2),
+ * through the LSU path (mode 0), the TEX path (1) or both at once (2). */
+int hrt_gather_peak(hrt_handle* h, int32_t mode, double* gbs);
+
 /* New world-space face geometry (same topology; host pointers). */
 int hrt_refit(hrt_handle* h, const double* v0, const double* e1, const double* e2,
               const double* normal, const double* bv0, const double* be1, const double* be2);

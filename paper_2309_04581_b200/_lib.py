@@ -102,6 +102,7 @@ SIGNATURES = {
                                        ctypes.c_int32, vp, vp]),
     "hrt_set_trace": (ctypes.c_int, [vp, vp, ctypes.c_int64]),
     "hrt_set_profile": (ctypes.c_int, [vp, ctypes.c_int32]),
+    "hrt_gather_peak": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
     "hrt_refit": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "hrt_field_sample": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, vp]),
     "hrt_field_encode": (ctypes.c_int, [vp, vp, ctypes.c_int64, vp, vp, vp]),

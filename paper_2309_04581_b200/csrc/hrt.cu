@@ -13,6 +13,7 @@
 #include "../../include/hrt.h"
 #include "bvh_build.h"
 #include "kernels.cuh"
+#include "probe.cuh"
 
 namespace {
 
@@ -88,6 +89,7 @@ struct hrt_handle {
     uint32_t* occ_dev = nullptr;
     int64_t occ_words = 0;
     unsigned long long tex = 0;
+    int64_t tab_entries = 0;
     // hrt_set_profile: event pair per launch, folded into stage_ms
     bool prof = false;
     std::vector<cudaEvent_t> pev;
@@ -319,6 +321,7 @@ int setup_field(hrt_handle* h, const hrt_field_desc& fd) {
         }
         float* table;
         if ((rc = h->upload(tab.data(), tab.size(), &table))) return rc;
+        h->tab_entries = padded;
         nf.table = table;
         {   // texture view of the table: the finest (incoherent) levels gather through the
             // TEX pipe of L1TEX, the rest through LSU, splitting the data-stage load
@@ -1027,6 +1030,58 @@ int hrt_primary_rays(const hrt_camera* cam, const int64_t* pixel, const int64_t*
     kern::k_primary<<<g, 256, 0, static_cast<cudaStream_t>(stream)>>>(to_cam(*cam), pixel, sample, n, seed,
                                                                       strat_of(spp), o, d);
     CK(cudaGetLastError());
+    return HRT_OK;
+}
+
+int hrt_gather_peak(hrt_handle* h, int32_t mode, double* gbs) {
+    if (!h || !gbs) return fail(HRT_EINVAL, "null argument");
+    if (h->sc.field.kind != HRT_FIELD_NEURAL || h->F != 2) return fail(HRT_EINVAL, "needs an F=2 neural field");
+    if (mode < 0 || mode > 2) return fail(HRT_EINVAL, "mode: 0 LSU, 1 TEX, 2 both");
+    const NeuralField& nf = h->sc.field.nf;
+    const uint32_t n = (uint32_t)h->tab_entries;
+    float* sink = nullptr;
+    CK(cudaMalloc(&sink, 4));
+    const int threads = 512, blocks = h->sm_count * 4, iters = 64;
+    const float2* tab = reinterpret_cast<const float2*>(nf.table);
+    cudaStream_t s2 = nullptr;
+    CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    auto launch = [&](cudaStream_t st, bool tex) {
+        if (tex) probe::k_gather<true><<<blocks, threads, 0, st>>>(tab, nf.tex, n, iters, sink);
+        else probe::k_gather<false><<<blocks, threads, 0, st>>>(tab, nf.tex, n, iters, sink);
+    };
+    auto run = [&]() {       // mode 2: LSU and TEX kernels side by side on two streams
+        if (mode == 2) {
+            CK(cudaEventRecord(h->ev0, 0));
+            CK(cudaStreamWaitEvent(s2, h->ev0, 0));
+            launch(0, false);
+            launch(s2, true);
+            CK(cudaEventRecord(h->ev1, s2));
+            CK(cudaStreamWaitEvent(0, h->ev1, 0));
+        } else {
+            launch(0, mode == 1);
+        }
+        return HRT_OK;
+    };
+    int rc;
+    if ((rc = run())) return rc;                       // warm (table into L2)
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, 0));
+    const int reps = 5;
+    for (int i = 0; i < reps; ++i)
+        if ((rc = run())) return rc;
+    CK(cudaEventRecord(e1, 0));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double loads = (double)blocks * threads * iters * 8 * reps * (mode == 2 ? 2 : 1);
+    *gbs = loads * 8.0 / (ms * 1e-3) / 1e9;            // useful bytes: 8 B per gather
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s2);
+    cudaFree(sink);
     return HRT_OK;
 }
 

@@ -159,6 +159,13 @@ class Renderer:
         """Per-stage device timing of later renders (last_stats['stage_ms'])."""
         _lib.check(self.lib.hrt_set_profile(self.handle, int(bool(on))), "hrt_set_profile")
 
+    def gather_peak(self, mode=2):
+        """Measured random 8-byte gather rate (useful GB/s) over this scene's
+        hash table: the roofline of the encode (hrt_gather_peak)."""
+        v = ctypes.c_double(0.0)
+        _lib.check(self.lib.hrt_gather_peak(self.handle, int(mode), ctypes.byref(v)), "hrt_gather_peak")
+        return v.value
+
     def set_trace(self, records, cap):
         _lib.check(self.lib.hrt_set_trace(self.handle, _dptr(records), int(cap)), "hrt_set_trace")
 
