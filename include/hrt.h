@@ -132,6 +132,7 @@ typedef struct {
     int64_t evaluated;            /* field evaluations incl. speculative ones discarded by early-out */
     int64_t rounds;               /* march rounds (generate -> field -> composite) */
     float stage_ms[8];            /* per-stage device time (HRT_STAGE_*), only after hrt_set_profile(h, 1) */
+    int64_t batch_rows;           /* field-engine rows launched (samples + holes) */
 } hrt_stats;
 
 /* Pipeline stages timed by hrt_set_profile (CUDA events around every launch). */
@@ -177,6 +178,18 @@ int hrt_set_trace(hrt_handle* h, int32_t* records, int64_t cap);
 /* Per-stage device timing of later hrt_render calls into hrt_stats.stage_ms
  * (on != 0) or off (default). Measurement aid: adds one event pair per launch. */
 int hrt_set_profile(hrt_handle* h, int32_t on);
+
+/* K9, finalize (render.py:399-401) on the device: hdr != 0 -> PFM bytes
+ * (images.py:37-40, float32 little-endian, rows bottom-up), else PPM P6
+ * (images.py:59-64, sRGB tone map core.py:51-64, round-half-up 8 bit).
+ * src: device float64 (n, 3) radiance rows; pixel: device int32 global pixel
+ * id per row (< 0 = padding), or NULL for a raster frame (n = w*h). This is
+ * also the unpack of the multi-GPU gather (rows = concatenated rank buffers).
+ * out: device buffer of cap bytes, or NULL to query *nbytes. Non-finite
+ * radiance in PPM mode -> HRT_ENONFINITE (reference tone_map asserts finite
+ * input); PFM stores it as is, like encode_pfm. */
+int hrt_finalize(int32_t width, int32_t height, const double* src, const int32_t* pixel, int64_t n,
+                 int32_t hdr, uint8_t* out, int64_t cap, int64_t* nbytes, void* stream);
 
 /* Roofline probe of the hash-grid encode: useful GB/s (8 B per gather) of
  * independent random 8-byte gathers over this scene's hash table (F = 2),

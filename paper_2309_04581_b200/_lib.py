@@ -75,7 +75,8 @@ class Stats(ctypes.Structure):
                 ("trace_records", ctypes.c_int64), ("ms", ctypes.c_float),
                 ("field_ms", ctypes.c_float), ("field_launches", ctypes.c_int32),
                 ("launches", ctypes.c_int64), ("evaluated", ctypes.c_int64),
-                ("rounds", ctypes.c_int64), ("stage_ms", ctypes.c_float * 8)]
+                ("rounds", ctypes.c_int64), ("stage_ms", ctypes.c_float * 8),
+                ("batch_rows", ctypes.c_int64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}
@@ -102,6 +103,8 @@ SIGNATURES = {
                                        ctypes.c_int32, vp, vp]),
     "hrt_set_trace": (ctypes.c_int, [vp, vp, ctypes.c_int64]),
     "hrt_set_profile": (ctypes.c_int, [vp, ctypes.c_int32]),
+    "hrt_finalize": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, vp, vp, ctypes.c_int64, ctypes.c_int32,
+                                    vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64), vp]),
     "hrt_gather_peak": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
     "hrt_refit": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "hrt_field_sample": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, vp]),

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -14,6 +15,7 @@
 #include "bvh_build.h"
 #include "kernels.cuh"
 #include "probe.cuh"
+#include "finalize.cuh"
 
 namespace {
 
@@ -80,6 +82,8 @@ struct hrt_handle {
     int64_t batch_cap = 0;
     int32_t* pinned = nullptr;
     int64_t rounds = 0;
+    int64_t batch_rows = 0;
+    bool debug_rounds = std::getenv("HRT_DEBUG_ROUNDS") != nullptr;
     int64_t io_cap = 0;
     int32_t *io_pix = nullptr, *io_pix_host = nullptr;
     double *io_out = nullptr, *io_out_host = nullptr;
@@ -547,6 +551,23 @@ int read_counters2(hrt_handle* h, int i0, int i1, cudaStream_t st, int32_t* v0, 
     return HRT_OK;
 }
 
+// Samples per path of a march round: kRoundSamples, raised for small (tail)
+// rounds so a batch still fills ~kTailTiles 128-row tiles per SM, capped by
+// the batch buffer.
+#ifndef HRT_TAIL_TILES
+#define HRT_TAIL_TILES 8
+#endif
+constexpr int64_t kTailTiles = HRT_TAIL_TILES;
+constexpr int64_t kMaxRoundSamples = 256;
+int32_t round_samples(const hrt_handle* h, int64_t live) {
+    int64_t S = kern::kRoundSamples;
+    if (kTailTiles > 0) {
+        const int64_t want = (int64_t)h->sm_count * 128 * kTailTiles / std::max<int64_t>(live, 1);
+        S = std::max<int64_t>(S, std::min<int64_t>(want, kMaxRoundSamples));
+    }
+    return (int32_t)std::max<int64_t>(1, std::min<int64_t>(S, h->batch_cap / std::max<int64_t>(live, 1)));
+}
+
 // ---- stage profiler (hrt_set_profile): pbeg/pend bracket one launch
 constexpr int kProfPairs = 4096;
 
@@ -589,8 +610,7 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
         // fused rounds: k_step (composite previous batch + generate) -> field -> shadow
         int32_t prev_nq = 0;
         for (int first = 1;; first = 0) {
-            const int32_t S = (int32_t)std::max<int64_t>(
-                1, std::min<int64_t>(kern::kRoundSamples, h->batch_cap / live));
+            const int32_t S = round_samples(h, live);
             pbeg(h, st);
             kern::k_round_reset<<<1, 1, 0, st>>>(h->ps.counters, mc ^ 1);
             kern::k_step<<<grid_for(h, live), kThreads, 0, st>>>(a, h->ms, mc, S, prev_nq, first);
@@ -603,6 +623,10 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
             // the batch: nxt continuing paths x S rows at stride `live`
             const fws::RowMap rm{live, nxt};
             const int64_t rows = (int64_t)nxt * S;
+            h->batch_rows += rows;
+            if (h->debug_rounds)
+                fprintf(stderr, "hrt round: bounce %d live %d next %d S %d rows %lld samples %d\n", a.bounce,
+                        live, nxt, S, (long long)rows, ns);
             pbeg(h, st);
             if ((rc = field_ws(h, h->ms.in, rm, rows, h->ms.dir32, h->ms.out, 0, st))) return rc;
             pend(h, HRT_STAGE_FIELD, st);
@@ -829,6 +853,7 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
     h->n_timed = 0;
     h->launches = 0;
     h->rounds = 0;
+    h->batch_rows = 0;
     h->pn = 0;
     for (double& x : h->stage_ms) x = 0.0;
     CK(cudaEventRecord(h->ev0, st));
@@ -890,6 +915,7 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
         stats->field_launches = h->n_timed;
         stats->launches = h->launches;
         for (int i = 0; i < 8; ++i) stats->stage_ms[i] = (float)h->stage_ms[i];
+        stats->batch_rows = h->batch_rows;
     }
     if (ctr[C_NONFINITE] != 0) return fail(HRT_ENONFINITE, "non-finite or negative radiance in frame");
     return HRT_OK;
@@ -1030,6 +1056,35 @@ int hrt_primary_rays(const hrt_camera* cam, const int64_t* pixel, const int64_t*
     kern::k_primary<<<g, 256, 0, static_cast<cudaStream_t>(stream)>>>(to_cam(*cam), pixel, sample, n, seed,
                                                                       strat_of(spp), o, d);
     CK(cudaGetLastError());
+    return HRT_OK;
+}
+
+int hrt_finalize(int32_t width, int32_t height, const double* src, const int32_t* pixel, int64_t n,
+                 int32_t hdr, uint8_t* out, int64_t cap, int64_t* nbytes, void* stream) {
+    if (width < 1 || height < 1 || !nbytes || (n > 0 && !src)) return fail(HRT_EINVAL, "bad arguments");
+    if (!pixel && n != (int64_t)width * height) return fail(HRT_EINVAL, "raster source needs w*h rows");
+    char head[64];
+    const int hl = hdr ? std::snprintf(head, sizeof(head), "PF\n%d %d\n-1.0\n", width, height)
+                       : std::snprintf(head, sizeof(head), "P6\n%d %d\n255\n", width, height);
+    const int64_t total = hl + (int64_t)width * height * 3 * (hdr ? 4 : 1);
+    *nbytes = total;
+    if (!out) return HRT_OK;                         // size query
+    if (cap < total) return fail(HRT_EINVAL, "output buffer too small");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int32_t* bad = nullptr;
+    CK(cudaMallocAsync(&bad, 4, st));
+    CK(cudaMemsetAsync(bad, 0, 4, st));
+    CK(cudaMemcpyAsync(out, head, hl, cudaMemcpyHostToDevice, st));
+    if (n > 0) {
+        const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
+        fin::k_finalize<<<g, 256, 0, st>>>(width, height, src, pixel, n, hdr, hl, out, bad);
+        CK(cudaGetLastError());
+    }
+    int32_t nb = 0;
+    CK(cudaMemcpyAsync(&nb, bad, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(bad, st));
+    CK(cudaStreamSynchronize(st));
+    if (nb) return fail(HRT_ENONFINITE, "finalize requires finite radiance");
     return HRT_OK;
 }
 

@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .images import HdrImage, encode_pfm, encode_ppm
+from .images import HdrImage
 from .pack import pack_camera, pack_scene, stratify_k  # noqa: F401  (re-export)
 
 
@@ -255,6 +255,26 @@ def trace_path(ray, scene, path_rng) -> np.ndarray:
     return r.trace(o, d, pix, smp, int(path_rng.seed)).cpu().numpy()[0]
 
 
+def finalize_device(src, width, height, hdr_output, pixel=None):
+    """K9 on the device: encoded PFM / PPM bytes (uint8 CUDA tensor) of float64
+    radiance rows `src` (n, 3); `pixel` (int32, < 0 = padding) gives each
+    row's global pixel id, None means `src` is the raster frame
+    (hrt_finalize)."""
+    lib = _lib.load()
+    src = src.contiguous()
+    n = int(src.shape[0])
+    nb = ctypes.c_int64(0)
+    args = (int(width), int(height), _dptr(src), _dptr(pixel) if pixel is not None else None, n,
+            int(bool(hdr_output)))
+    _lib.check(lib.hrt_finalize(*args, None, 0, ctypes.byref(nb), _stream()), "hrt_finalize")
+    out = torch.empty(nb.value, dtype=torch.uint8, device=src.device)
+    _lib.check(lib.hrt_finalize(*args, _dptr(out), nb.value, ctypes.byref(nb), _stream()),
+               "hrt_finalize")
+    return out
+
+
 def finalize(img: HdrImage, hdr_output: bool) -> bytes:
-    """PFM bytes for HDR output, else tone-mapped 8-bit PPM (render.py:399-401)."""
-    return encode_pfm(img) if hdr_output else encode_ppm(img)
+    """PFM bytes for HDR output, else tone-mapped 8-bit PPM (render.py:399-401),
+    encoded on the GPU (K9)."""
+    px = torch.as_tensor(np.ascontiguousarray(img.pixels, np.float64).reshape(-1, 3), device="cuda")
+    return finalize_device(px, img.w, img.h, hdr_output).cpu().numpy().tobytes()

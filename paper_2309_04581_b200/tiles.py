@@ -45,6 +45,12 @@ class FrameGather:
         self.index = [torch.as_tensor(tile_pixels(w, h, q, world).astype(np.int64), device=device)
                       for q in range(world)]
         self.frame = torch.zeros((w * h, 3), dtype=dtype, device=device) if rank == 0 else None
+        # global pixel id of every row of the concatenated rank buffers (-1 = padding)
+        pad = np.full((world, self.n_max), -1, np.int32)
+        for q in range(world):
+            ids = tile_pixels(w, h, q, world)
+            pad[q, :len(ids)] = ids
+        self.row_pixel = torch.as_tensor(pad.reshape(-1), device=device)
 
     def gather(self):
         import torch.distributed as dist
@@ -58,3 +64,19 @@ class FrameGather:
                 n = len(self.index[q])
                 self.frame.index_copy_(0, self.index[q], parts[q][:n])
         return self.frame
+
+    def finalize(self, hdr_output):
+        """All-gather, then unpack + encode (PFM / PPM, K9 hrt_finalize) in one
+        device pass over the rank buffers on rank 0; returns the file bytes
+        (rank 0) or None."""
+        import torch
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.all_gather(self.parts, self.local, group=self.group)
+            rows = torch.cat(self.parts)
+        else:
+            rows = self.local
+        if self.rank != 0:
+            return None
+        from .renderer import finalize_device
+        return finalize_device(rows, self.w, self.h, hdr_output, pixel=self.row_pixel).cpu().numpy().tobytes()

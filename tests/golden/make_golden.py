@@ -9,6 +9,8 @@ pin both the CPU oracle (tests/test_golden.py, not gpu) and the CUDA path
   rays.npz    _sample_jitter + Camera.primary_rays, 3 cameras   (render.py:61-74, 320-330)
   bvh.npz     Bvh.intersect_batch / any_hit_batch, 2 meshes      (surface.py:377-478)
   field.npz   RadianceGrid.sample_batch incl. outside / borders  (field.py:143-161)
+  images.npz  finalize -> encode_ppm / encode_pfm bytes of 3 HDR frames incl. the sRGB
+              cut, the 1.0 rail, > 1, zeros and tiny values   (render.py:399-401, images.py:37-64)
   render.npz  render / render_surface_only / render_volume_only on dense-grid scenes
               (mirror fog, glass fog, Lambertian room, shadowed slab), with every
               input array needed to rebuild the scenes without the reference.
@@ -26,6 +28,8 @@ sys.path.insert(0, "/root/reference/pkg/src")
 from hybridrt import assets, rng  # noqa: E402
 from hybridrt.core import Transform  # noqa: E402
 from hybridrt.field import RadianceGrid  # noqa: E402
+from hybridrt.images import HdrImage  # noqa: E402
+from hybridrt.render import finalize  # noqa: E402
 from hybridrt.render import (Camera, EmitterSet, _sample_jitter, render,  # noqa: E402
                              render_surface_only, render_volume_only)
 from hybridrt.scene import CameraConfig, RenderConfig, Scene, SceneConfig, scene_diagonal  # noqa: E402
@@ -108,6 +112,23 @@ def dense_field(seed):
     return g.uniform(0.5, 1.5, (8, 9, 10)), g.uniform(0, 1, (8, 9, 10, 3))
 
 
+
+def gen_images():
+    g = np.random.default_rng(5)
+    frames = [g.uniform(0.0, 1.0, (9, 13, 3)),
+              np.exp(g.normal(-2.0, 2.0, (16, 16, 3))),                  # HDR, spans 1e-4 .. 50
+              np.zeros((4, 5, 3))]
+    special = np.array([0.0, 0.0031308, np.nextafter(0.0031308, 1), 1.0, np.nextafter(1.0, 0),
+                        1.5, 1e-300, 5e-324, 0.5, 0.21404114048223255, 1e6, 0.99999])
+    frames[2].reshape(-1)[:len(special)] = special
+    out = {}
+    for i, f in enumerate(frames):
+        img = HdrImage(f)
+        out[f"px{i}"] = f
+        out[f"ppm{i}"] = np.frombuffer(finalize(img, False), np.uint8)
+        out[f"pfm{i}"] = np.frombuffer(finalize(img, True), np.uint8)
+    np.savez_compressed(os.path.join(OUT, "images.npz"), **out)
+
 def gen_render():
     out = {}
     v, f = assets.icosphere(0.4, 2)
@@ -157,6 +178,7 @@ if __name__ == "__main__":
     gen_rays()
     gen_bvh()
     gen_field()
+    gen_images()
     gen_render()
     for fn in sorted(os.listdir(OUT)):
         if fn.endswith(".npz"):

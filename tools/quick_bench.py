@@ -29,6 +29,6 @@ for it in range(int(sys.argv[4]) if len(sys.argv) > 4 else 4):
     print(f"iter {it}: wall {dt*1e3:.1f} ms dev {s['ms']:.1f} ms samples {s['nerf_samples']:,} "
           f"({s['nerf_samples']/s['ms']*1e3/1e9:.3f} G/s) paths {s['paths']:,} "
           f"Mrays/s {s['paths']/s['ms']*1e3/1e6:.2f} mean {out.mean().item():.4f} | field {s['field_ms']:.1f} ms "
-          f"x{s['field_launches']} evaluated {s['evaluated']:,} rounds {s['rounds']} launches {s['launches']}",
+          f"x{s['field_launches']} evaluated {s['evaluated']:,} rounds {s['rounds']} launches {s['launches']} rows {s['batch_rows']:,}",
           flush=True)
     print("   stages ms: " + " ".join(f"{k}={v:.1f}" for k, v in s["stage_ms"].items()), flush=True)
