@@ -169,7 +169,7 @@ struct PathState {
                                               // frame evaluates ~1e11 NeRF samples
 };
 
-enum Stat { S_SAMPLES = 0, S_SHADOW = 1, S_SEGMENTS = 2, S_EVALS = 3, S_COUNT = 8 };
+enum Stat { S_SAMPLES = 0, S_SHADOW = 1, S_SEGMENTS = 2, S_EVALS = 3, S_ROWS = 4, S_COUNT = 8 };
 
 HRT_DEV void stat_add(unsigned long long* stats, int which, long long v) {
     atomicAdd(stats + which, (unsigned long long)v);
@@ -177,6 +177,10 @@ HRT_DEV void stat_add(unsigned long long* stats, int which, long long v) {
 
 enum Counter { C_Q0 = 0, C_Q1 = 1, C_FETCH = 2,
                C_NONFINITE = 6, C_TRACE = 7, C_MQ0 = 8, C_MQ1 = 9, C_NS = 10,
+               // device-driven march rounds (k_round_begin): current march queue,
+               // first-round flag, samples per path, row stride of this and the
+               // previous batch
+               C_CUR = 12, C_FIRST = 13, C_S = 14, C_STRIDE = 15, C_PSTRIDE = 16,
                C_COUNT = 16 };
 
 HRT_DEV d3 field_point(const DevField& f, d3 p) {

@@ -138,7 +138,8 @@ __device__ __forceinline__ void relu64_tmem(uint32_t accum, uint32_t act) {
 template <int E, int F>
 __global__ void __launch_bounds__(kThreads, 1)
 k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t n,
-           const float4* __restrict__ dir32, float4* __restrict__ out, int32_t density_only) {
+           const float4* __restrict__ dir32, float4* __restrict__ out, int32_t density_only,
+           const int32_t* __restrict__ round_ctr, unsigned long long* stats) {
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr SmemPlan P = plan(E);
     constexpr nerf::WOff W = nerf::woff(E);
@@ -147,6 +148,13 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
     constexpr int NC = NL * F / 2;                // TMEM columns per encode thread
     constexpr uint32_t kStageCols = E / 2;
     const int warp = threadIdx.x >> 5;
+    if (round_ctr) {                 // device-driven march round (kern::k_round_begin counters)
+        rmap.width = round_ctr[C_MQ0 + (round_ctr[C_CUR] ^ 1)];
+        rmap.stride = round_ctr[C_STRIDE];
+        n = (int64_t)rmap.width * round_ctr[C_S];
+        if (blockIdx.x == 0 && threadIdx.x == 0 && stats) atomicAdd(stats + S_ROWS, (unsigned long long)n);
+    }
+    if (n <= 0) return;              // empty round: skip the prologue
     const int64_t tiles = (n + kRows - 1) / kRows;
 
     // ---- prologue: weights to smem, barriers, TMEM

@@ -83,7 +83,6 @@ struct hrt_handle {
     int32_t* pinned = nullptr;
     int64_t rounds = 0;
     int64_t batch_rows = 0;
-    bool debug_rounds = std::getenv("HRT_DEBUG_ROUNDS") != nullptr;
     int64_t io_cap = 0;
     int32_t *io_pix = nullptr, *io_pix_host = nullptr;
     double *io_out = nullptr, *io_out_host = nullptr;
@@ -378,13 +377,14 @@ unsigned grid_for(const hrt_handle* h, int64_t n) {
 
 template <int E, int F>
 int launch_ws(hrt_handle* h, const fws::SampleIn* in, fws::RowMap rm, int64_t n, const float4* dir32,
-              float4* out, int density_only, cudaStream_t st) {
+              float4* out, int density_only, const int32_t* round_ctr, cudaStream_t st) {
     constexpr uint32_t smem = fws::plan(E).total;
     CK(cudaFuncSetAttribute(fws::k_field_ws<E, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t tiles = (n + fws::kRows - 1) / fws::kRows;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)h->sm_count));
+    const int grid = round_ctr ? h->sm_count
+                               : (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)h->sm_count));
     fws::k_field_ws<E, F><<<grid, fws::kThreads, smem, st>>>(h->sc.field.nf, in, rm, n, dir32, out,
-                                                             density_only);
+                                                             density_only, round_ctr, h->ps.stats);
     CK(cudaGetLastError());
     return HRT_OK;
 }
@@ -393,18 +393,18 @@ int launch_ws(hrt_handle* h, const fws::SampleIn* in, fws::RowMap rm, int64_t n,
 // field engine; bracketed by events so the dominant kernel's device time is
 // measured live.
 int field_ws(hrt_handle* h, const fws::SampleIn* in, fws::RowMap rm, int64_t n, const float4* dir32,
-             float4* out, int density_only, cudaStream_t st) {
-    if (n <= 0) return HRT_OK;
+             float4* out, int density_only, cudaStream_t st, const int32_t* round_ctr = nullptr) {
+    if (n <= 0 && !round_ctr) return HRT_OK;
     const bool timed = h->n_timed < kTimedLaunches;
     if (timed) CK(cudaEventRecord(h->mev[2 * h->n_timed], st));
     int rc;
     switch (h->E * 8 + h->F) {
-        case 16 * 8 + 2: rc = launch_ws<16, 2>(h, in, rm, n, dir32, out, density_only, st); break;
-        case 32 * 8 + 2: rc = launch_ws<32, 2>(h, in, rm, n, dir32, out, density_only, st); break;
-        case 64 * 8 + 4: rc = launch_ws<64, 4>(h, in, rm, n, dir32, out, density_only, st); break;
-        case 32 * 8 + 4: rc = launch_ws<32, 4>(h, in, rm, n, dir32, out, density_only, st); break;
-        case 64 * 8 + 2: rc = launch_ws<64, 2>(h, in, rm, n, dir32, out, density_only, st); break;
-        case 16 * 8 + 4: rc = launch_ws<16, 4>(h, in, rm, n, dir32, out, density_only, st); break;
+        case 16 * 8 + 2: rc = launch_ws<16, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
+        case 32 * 8 + 2: rc = launch_ws<32, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
+        case 64 * 8 + 4: rc = launch_ws<64, 4>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
+        case 32 * 8 + 4: rc = launch_ws<32, 4>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
+        case 64 * 8 + 2: rc = launch_ws<64, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
+        case 16 * 8 + 4: rc = launch_ws<16, 4>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
         default: return fail(HRT_EINVAL, "unsupported encoding width");
     }
     if (rc) return rc;
@@ -542,15 +542,6 @@ int read_counter(hrt_handle* h, int idx, cudaStream_t st, int32_t* v) {
     return HRT_OK;
 }
 
-int read_counters2(hrt_handle* h, int i0, int i1, cudaStream_t st, int32_t* v0, int32_t* v1) {
-    CK(cudaMemcpyAsync(h->pinned, h->ps.counters + i0, 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h->pinned + 1, h->ps.counters + i1, 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    *v0 = h->pinned[0];
-    *v1 = h->pinned[1];
-    return HRT_OK;
-}
-
 // Samples per path of a march round: kRoundSamples, raised for small (tail)
 // rounds so a batch still fills ~kTailTiles 128-row tiles per SM, capped by
 // the batch buffer.
@@ -558,7 +549,11 @@ int read_counters2(hrt_handle* h, int i0, int i1, cudaStream_t st, int32_t* v0, 
 #define HRT_TAIL_TILES 8
 #endif
 constexpr int64_t kTailTiles = HRT_TAIL_TILES;
-constexpr int64_t kMaxRoundSamples = 256;
+constexpr int64_t kMaxRoundSamples = 256;      // (k_round_begin uses the same 256)
+#ifndef HRT_ROUNDS_PER_CHECK
+#define HRT_ROUNDS_PER_CHECK 2
+#endif
+constexpr int kRoundsPerCheck = HRT_ROUNDS_PER_CHECK;
 int32_t round_samples(const hrt_handle* h, int64_t live) {
     int64_t S = kern::kRoundSamples;
     if (kTailTiles > 0) {
@@ -595,6 +590,52 @@ inline void pend(hrt_handle* h, int stage, cudaStream_t st) {
 // k_gen -> k_field_ws -> k_comp until no path has midpoints left.
 int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream_t st) {
     const unsigned g = grid_for(h, n_paths);
+    int rc;
+    if (!a.trace) {
+        // Device-driven fused rounds, no host sync per round:
+        //   k_round_begin (queue flip, S, strides) -> k_step (composite the
+        //   previous batch + generate the next) -> field engine -> shadows,
+        // every kernel reading the round's shape from the device counters.
+        // Rounds are enqueued kRoundsPerCheck at a time; the host then checks
+        // whether the last round generated any sample (rounds after the end
+        // are empty launches).
+        pbeg(h, st);
+        kern::k_march_begin<<<1, 1, 0, st>>>(h->ps.counters);
+        kern::k_seg<<<g, kThreads, 0, st>>>(a, h->ms);
+        CK(cudaGetLastError());
+        pend(h, HRT_STAGE_MARCH_GEN, st);
+        h->launches += 2;
+        const int32_t target = (int32_t)std::min<int64_t>((int64_t)h->sm_count * 128 * kTailTiles, 1 << 30);
+        const int32_t cap = (int32_t)std::min<int64_t>(h->batch_cap, 1 << 30);
+        const unsigned gsh = (unsigned)(h->sm_count * 16);
+        while (true) {
+            for (int k = 0; k < kRoundsPerCheck; ++k) {
+                pbeg(h, st);
+                kern::k_round_begin<<<1, 1, 0, st>>>(h->ps.counters, h->ps.stats, target, cap);
+                kern::k_step<<<g, kThreads, 0, st>>>(a, h->ms);
+                CK(cudaGetLastError());
+                pend(h, HRT_STAGE_COMPOSITE, st);
+                pbeg(h, st);
+                if ((rc = field_ws(h, h->ms.in, fws::RowMap{0, 0}, 0, h->ms.dir32, h->ms.out, 0, st,
+                                   h->ps.counters)))
+                    return rc;
+                pend(h, HRT_STAGE_FIELD, st);
+                if (h->sc.em.n > 0) {
+                    pbeg(h, st);
+                    kern::k_shadow<<<gsh, kThreads, 0, st>>>(a, h->ms, fws::RowMap{0, 0}, 0, 1);
+                    CK(cudaGetLastError());
+                    pend(h, HRT_STAGE_SHADOW, st);
+                    ++h->launches;
+                }
+                h->launches += 2;
+                ++h->rounds;
+            }
+            int32_t ns = 0;
+            if ((rc = read_counter(h, C_NS, st, &ns))) return rc;
+            if (ns == 0) break;
+        }
+        return HRT_OK;
+    }
     pbeg(h, st);
     kern::k_round_reset<<<1, 1, 0, st>>>(h->ps.counters, 0);
     kern::k_seg<<<g, kThreads, 0, st>>>(a, h->ms);
@@ -602,51 +643,10 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
     pend(h, HRT_STAGE_MARCH_GEN, st);
     h->launches += 2;
     int32_t live = 0;
-    int rc;
     if ((rc = read_counter(h, C_MQ0, st, &live))) return rc;
     int mc = 0;
-    if (live == 0) return HRT_OK;
-    if (!a.trace) {
-        // fused rounds: k_step (composite previous batch + generate) -> field -> shadow
-        int32_t prev_nq = 0;
-        for (int first = 1;; first = 0) {
-            const int32_t S = round_samples(h, live);
-            pbeg(h, st);
-            kern::k_round_reset<<<1, 1, 0, st>>>(h->ps.counters, mc ^ 1);
-            kern::k_step<<<grid_for(h, live), kThreads, 0, st>>>(a, h->ms, mc, S, prev_nq, first);
-            CK(cudaGetLastError());
-            pend(h, HRT_STAGE_COMPOSITE, st);
-            h->launches += 2;
-            int32_t nxt = 0, ns = 0;
-            if ((rc = read_counters2(h, C_MQ0 + (mc ^ 1), C_NS, st, &nxt, &ns))) return rc;
-            if (ns == 0) break;
-            // the batch: nxt continuing paths x S rows at stride `live`
-            const fws::RowMap rm{live, nxt};
-            const int64_t rows = (int64_t)nxt * S;
-            h->batch_rows += rows;
-            if (h->debug_rounds)
-                fprintf(stderr, "hrt round: bounce %d live %d next %d S %d rows %lld samples %d\n", a.bounce,
-                        live, nxt, S, (long long)rows, ns);
-            pbeg(h, st);
-            if ((rc = field_ws(h, h->ms.in, rm, rows, h->ms.dir32, h->ms.out, 0, st))) return rc;
-            pend(h, HRT_STAGE_FIELD, st);
-            if (h->sc.em.n > 0) {
-                pbeg(h, st);
-                kern::k_shadow<<<grid_for(h, rows), kThreads, 0, st>>>(a, h->ms, rm, rows);
-                CK(cudaGetLastError());
-                pend(h, HRT_STAGE_SHADOW, st);
-                ++h->launches;
-            }
-            ++h->rounds;
-            prev_nq = live;
-            live = nxt;
-            mc ^= 1;
-        }
-        return HRT_OK;
-    }
     while (live > 0) {
-        const int32_t S = (int32_t)std::max<int64_t>(
-            1, std::min<int64_t>(kern::kRoundSamples, h->batch_cap / live));
+        const int32_t S = round_samples(h, live);
         const unsigned gl = grid_for(h, live);
         pbeg(h, st);
         kern::k_round_reset<<<1, 1, 0, st>>>(h->ps.counters, mc ^ 1);
@@ -661,7 +661,7 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
         if (h->sc.em.n > 0) {
             const int64_t rows = (int64_t)live * S;
             pbeg(h, st);
-            kern::k_shadow<<<grid_for(h, rows), kThreads, 0, st>>>(a, h->ms, fws::RowMap{0, 0}, rows);
+            kern::k_shadow<<<grid_for(h, rows), kThreads, 0, st>>>(a, h->ms, fws::RowMap{0, 0}, rows, 0);
             CK(cudaGetLastError());
             pend(h, HRT_STAGE_SHADOW, st);
             ++h->launches;
@@ -915,7 +915,7 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
         stats->field_launches = h->n_timed;
         stats->launches = h->launches;
         for (int i = 0; i < 8; ++i) stats->stage_ms[i] = (float)h->stage_ms[i];
-        stats->batch_rows = h->batch_rows;
+        stats->batch_rows = h->batch_rows + (int64_t)tot[S_ROWS];
     }
     if (ctr[C_NONFINITE] != 0) return fail(HRT_ENONFINITE, "non-finite or negative radiance in frame");
     return HRT_OK;

@@ -472,9 +472,10 @@ __global__ void __launch_bounds__(256, HRT_COMP_MINB) k_comp(Args a, MarchState 
 // generates its next samples at rows i * nq + r. One pass over the path
 // state per round instead of two (k_gen + k_comp); a path whose remaining
 // candidates are all empty cells keeps a rank with S hole rows.
-__global__ void __launch_bounds__(256, 1) k_step(Args a, MarchState m, int32_t mcur, int32_t S,
-                                               int32_t prev_nq, int32_t first) {
-    const int32_t nq = a.ps.counters[C_MQ0 + mcur];
+__global__ void __launch_bounds__(256, 1) k_step(Args a, MarchState m) {
+    const int32_t* ctr = a.ps.counters;
+    const int32_t mcur = ctr[C_CUR], S = ctr[C_S], prev_nq = ctr[C_PSTRIDE], first = ctr[C_FIRST];
+    const int32_t nq = ctr[C_MQ0 + mcur];
     const int32_t* q = pick(m.mq, mcur);
     int32_t* next = pick(m.mq, mcur ^ 1);
     int32_t* next_n = &a.ps.counters[C_MQ0 + (mcur ^ 1)];
@@ -510,8 +511,14 @@ __global__ void __launch_bounds__(256, 1) k_step(Args a, MarchState m, int32_t m
 // traces the shadow rays of 32 neighbouring pixels at the same step). Rows
 // that cannot contribute (opacity 0 or black) cast no ray, as in the
 // reference (field.py:246-251).
-__global__ void k_shadow(Args a, MarchState m, fws::RowMap rm, int64_t rows) {
+__global__ void k_shadow(Args a, MarchState m, fws::RowMap rm, int64_t rows, int32_t dev_rows) {
     const PathState& s = a.ps;
+    if (dev_rows) {                  // device-driven round: this round's batch shape
+        const int32_t* ctr = a.ps.counters;
+        rm.width = ctr[C_MQ0 + (ctr[C_CUR] ^ 1)];
+        rm.stride = ctr[C_STRIDE];
+        rows = (int64_t)rm.width * ctr[C_S];
+    }
     int32_t cast = 0;
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < rows;
          l += (int64_t)gridDim.x * blockDim.x) {
@@ -534,6 +541,36 @@ __global__ void k_shadow(Args a, MarchState m, fws::RowMap rm, int64_t rows) {
         m.shadow[row] = code;
     }
     if (cast) stat_add(a.ps.stats, S_SHADOW, cast);
+}
+
+// Device-driven march round (no host sync): flip to the queue k_step will
+// read, fix its samples per path (kRoundSamples, more for small tail rounds,
+// capped by the batch buffer) and the batch strides, empty the next queue.
+__global__ void k_round_begin(int32_t* c, unsigned long long* stats, int32_t target_rows,
+                              int32_t batch_cap) {
+    const int32_t cur = c[C_CUR] ^ 1;
+    c[C_CUR] = cur;
+    c[C_FIRST] = c[C_FIRST] == 2 ? 1 : 0;       // 2 = set by k_march_begin
+    const int32_t live = c[C_MQ0 + cur];
+    int32_t S = kRoundSamples;
+    if (live > 0) {
+        S = max(S, min(target_rows / live, 256));
+        S = max(1, min(S, batch_cap / live));
+    }
+    c[C_S] = S;
+    c[C_PSTRIDE] = c[C_STRIDE];
+    c[C_STRIDE] = live;
+    c[C_MQ0 + (cur ^ 1)] = 0;
+    c[C_NS] = 0;
+    (void)stats;
+}
+
+// Before the first round of a bounce (k_seg fills march queue 0).
+__global__ void k_march_begin(int32_t* c) {
+    c[C_CUR] = 1;                // k_round_begin flips it to 0
+    c[C_FIRST] = 2;
+    c[C_MQ0] = 0;
+    c[C_STRIDE] = 0;
 }
 
 // Start of a march round: empty the batch and the next march queue.
