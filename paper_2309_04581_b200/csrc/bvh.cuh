@@ -260,6 +260,17 @@ HRT_DEV int32_t closest_w(const DevBvh& b, d3 o, d3 d, double t_min, double t_ma
     return best_f;
 }
 
+// Can the segment reach any box of the tree at all? (root WNode's children)
+HRT_DEV bool root_overlap(const DevBvh& b, d3 o, d3 d, double t_min, double t_max) {
+    if (b.n_faces == 0) return false;
+    const Ray32 r = prep32(o, d);
+    const WNode w = load_w(b.wnodes, 0);
+    bool h0, h1;
+    float n0, n1;
+    wchildren(w, r, t_lo32(t_min), t_hi32(t_max), h0, h1, n0, n1);
+    return h0 || h1;
+}
+
 // True if any face lies in (t_min, t_max] (surface.py:442-478).
 HRT_DEV bool any_hit_w(const DevBvh& b, d3 o, d3 d, double t_min, double t_max) {
     if (b.n_faces == 0) return false;

@@ -51,6 +51,17 @@ HRT_DEV double uniform(uint64_t seed, int64_t pix, int64_t smp, int64_t bounce, 
     h = step(h, bounce); h = step(h, purpose); h = step(h, lane);
     return (double)(h >> 11) * (1.0 / 9007199254740992.0);
 }
+// The chain state after (seed, pix, smp, bounce): every draw of one path
+// segment shares it (shadow rays of a march: 3 draws per sample).
+HRT_DEV uint64_t prefix(uint64_t seed, int64_t pix, int64_t smp, int64_t bounce) {
+    uint64_t h = G;
+    h = step(h, (int64_t)seed); h = step(h, pix); h = step(h, smp);
+    return step(h, bounce);
+}
+HRT_DEV double uniform_from(uint64_t h4, int64_t purpose, int64_t lane) {
+    const uint64_t h = step(step(h4, purpose), lane);
+    return (double)(h >> 11) * (1.0 / 9007199254740992.0);
+}
 }  // namespace rng
 
 // ------------------------------------------------------------------ scene
@@ -181,6 +192,8 @@ enum Counter { C_Q0 = 0, C_Q1 = 1, C_FETCH = 2,
                // first-round flag, samples per path, row stride of this and the
                // previous batch
                C_CUR = 12, C_FIRST = 13, C_S = 14, C_STRIDE = 15, C_PSTRIDE = 16,
+               // shadow-ray queue of a round: length, fetch cursor of the tracer
+               C_SHQ = 17, C_SHF = 18,
                C_COUNT = 16 };
 
 HRT_DEV d3 field_point(const DevField& f, d3 p) {

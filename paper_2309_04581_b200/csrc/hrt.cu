@@ -36,6 +36,10 @@ int fail(int code, const std::string& msg) {
 constexpr int64_t kMaxPaths = int64_t(1) << 20;   // paths per wavefront chunk
 constexpr int kThreads = 256;
 constexpr int kTimedLaunches = 1024;
+#ifndef HRT_SHADOW_QUEUE
+#define HRT_SHADOW_QUEUE 1
+#endif
+constexpr bool kShadowQueue = HRT_SHADOW_QUEUE;   // shadow rays: set-up pass + persistent tracer
 constexpr int64_t kBatchCap = int64_t(1) << 24;   // samples per march round
 #ifndef HRT_TEX_LEVELS
 #define HRT_TEX_LEVELS 8
@@ -93,6 +97,7 @@ struct hrt_handle {
     int64_t occ_words = 0;
     unsigned long long tex = 0;
     int64_t tab_entries = 0;
+    int shadow_blocks = 0;
     // hrt_set_profile: event pair per launch, folded into stage_ms
     bool prof = false;
     std::vector<cudaEvent_t> pev;
@@ -257,6 +262,7 @@ int upload_bvh(hrt_handle* h, const hrt::BvhHost& b, DevBvh& out, int2** wsrc, i
     if ((rc = h->upload(b.tri.data(), b.tri.size(), &tri))) return rc;
     if ((rc = h->upload(b.tri_id.data(), b.tri_id.size(), &ids))) return rc;
     out.nodes = nodes; out.tri = tri; out.tri_id = ids;
+
     return HRT_OK;
 }
 
@@ -504,10 +510,13 @@ int ensure_state(hrt_handle* h, int64_t paths) {
         m.n = take_i(); m.k = take_i(); m.base = take_i(); m.cnt = take_i();
         m.mq[0] = take_i(); m.mq[1] = take_i();
         m.dir32 = reinterpret_cast<float4*>(take(f4));
+        m.h4 = reinterpret_cast<uint64_t*>(take(dbl));
         m.in = reinterpret_cast<fws::SampleIn*>(take((size_t)nb * 16));
         m.sk = reinterpret_cast<int32_t*>(take((size_t)nb * 4));
         m.out = reinterpret_cast<float4*>(take((size_t)nb * 16));
         m.shadow = reinterpret_cast<int32_t*>(take((size_t)nb * 4));
+        m.shq = (h->sc.em.n > 0 && kShadowQueue) ? reinterpret_cast<kern::QRay*>(take((size_t)nb * sizeof(kern::QRay)))
+                                                 : nullptr;
         s.counters = reinterpret_cast<int32_t*>(take(64 * 4));
         s.stats = reinterpret_cast<unsigned long long*>(take(S_COUNT * 8));
         if (pass == 0) CK(cudaMalloc(&h->arena, off));
@@ -586,6 +595,20 @@ inline void pend(hrt_handle* h, int stage, cudaStream_t st) {
     if (h->pn == kProfPairs) prof_fold(h, st);
 }
 
+// Queued shadow rays of the round through the blocker tree (persistent).
+int shadow_trace(hrt_handle* h, const kern::Args& a, cudaStream_t st) {
+    if (!h->ms.shq) return HRT_OK;
+    if (h->shadow_blocks == 0) {
+        int nb = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern::k_shadow_trace, 256, 0));
+        h->shadow_blocks = std::max(1, nb) * h->sm_count;
+    }
+    kern::k_shadow_trace<<<h->shadow_blocks, 256, 0, st>>>(a, h->ms);
+    CK(cudaGetLastError());
+    ++h->launches;
+    return HRT_OK;
+}
+
 // NeRF march of every alive path of this bounce: k_seg, then rounds of
 // k_gen -> k_field_ws -> k_comp until no path has midpoints left.
 int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream_t st) {
@@ -624,6 +647,7 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
                     pbeg(h, st);
                     kern::k_shadow<<<gsh, kThreads, 0, st>>>(a, h->ms, fws::RowMap{0, 0}, 0, 1);
                     CK(cudaGetLastError());
+                    if ((rc = shadow_trace(h, a, st))) return rc;
                     pend(h, HRT_STAGE_SHADOW, st);
                     ++h->launches;
                 }
@@ -663,6 +687,7 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
             pbeg(h, st);
             kern::k_shadow<<<grid_for(h, rows), kThreads, 0, st>>>(a, h->ms, fws::RowMap{0, 0}, rows, 0);
             CK(cudaGetLastError());
+            if ((rc = shadow_trace(h, a, st))) return rc;
             pend(h, HRT_STAGE_SHADOW, st);
             ++h->launches;
         }

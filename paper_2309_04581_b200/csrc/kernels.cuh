@@ -305,6 +305,15 @@ struct MarchState {         // per path, valid while the path is marching
     int32_t* sk;            // midpoint index of each batch sample
     float4* out;            // (sigma, rgb) of each batch sample
     int32_t* shadow;        // per batch sample: 0 visible / 1 + blocked emitter index
+    struct QRay* shq;       // shadow rays that reach the blocker tree (k_shadow_trace)
+    uint64_t* h4;           // per path: rng::prefix(seed, pix, smp, bounce) of this bounce
+};
+
+// A queued shadow ray (64 B): origin = the NeRF sample point, float64 as the
+// reference; row of the batch sample it decides.
+struct __align__(16) QRay {
+    double ox, oy, oz, dx, dy, dz, tmax;
+    int32_t row, idx;
 };
 
 __global__ void k_seg(Args a, MarchState m) {
@@ -322,6 +331,7 @@ __global__ void k_seg(Args a, MarchState m) {
         m.k[p] = 0;
         const d3 df = field_dir(a.sc.field, d);
         m.dir32[p] = make_float4((float)df.x, (float)df.y, (float)df.z, 0.f);
+        if (m.shq) m.h4[p] = rng::prefix(a.seed, s.pix[p], s.smp[p], a.bounce);
         m.mq[0][reserve(&a.ps.counters[C_MQ0])] = p;
     }
 }
@@ -534,13 +544,110 @@ __global__ void k_shadow(Args a, MarchState m, fws::RowMap rm, int64_t rows, int
             const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
             const Segment g{m.s0[p], delta, m.n[p]};
             const int32_t k = m.sk[row];
-            code = path::shadow_code(a.sc, sample_point(o, d, g, k), a.seed, s.pix[p], s.smp[p],
-                                     a.bounce, k);
+            const d3 x = sample_point(o, d, g, k);
+            if (m.shq) {
+                // queue the ray for k_shadow_trace unless it misses the blocker tree's root
+                const path::ShadowRay r = path::shadow_ray_h(a.sc, x, m.h4[p], k);
+                if (bvh::root_overlap(a.sc.blockers, x, r.dir, a.sc.spawn_eps, r.tmax)) {
+                    QRay q;
+                    q.ox = x.x; q.oy = x.y; q.oz = x.z;
+                    q.dx = r.dir.x; q.dy = r.dir.y; q.dz = r.dir.z;
+                    q.tmax = r.tmax;
+                    q.row = (int32_t)row;
+                    q.idx = r.idx;
+                    m.shq[reserve(&a.ps.counters[C_SHQ])] = q;
+                    code = -1;                         // decided by k_shadow_trace
+                }
+            } else {
+                code = path::shadow_code(a.sc, x, a.seed, s.pix[p], s.smp[p], a.bounce, k);
+            }
             ++cast;
         }
-        m.shadow[row] = code;
+        if (code >= 0) m.shadow[row] = code;
     }
     if (cast) stat_add(a.ps.stats, S_SHADOW, cast);
+}
+
+// Any-hit of the queued shadow rays: persistent warps that refill idle lanes
+// from the queue (warp-aggregated fetch once a quarter of the warp is idle)
+// and advance every lane one BVH node per iteration, so long traversals do
+// not hold the rest of the warp idle. Same culling and float64 triangle
+// tests as bvh::any_hit_w: the blocked / visible answer is identical.
+__global__ void __launch_bounds__(256) k_shadow_trace(Args a, MarchState m) {
+    const int32_t n = a.ps.counters[C_SHQ];
+    int32_t* fetch = &a.ps.counters[C_SHF];
+    const DevBvh& b = a.sc.blockers;
+    const uint32_t lane = threadIdx.x & 31;
+    const double t_min = a.sc.spawn_eps;
+    int32_t qi = -1;
+    bool exhausted = false;
+    d3 o{}, d{};
+    double tmax = 0.0;
+    bvh::Ray32 r32{};
+    float t0 = 0.f, t1 = 0.f;
+    int32_t stack[bvh::kStack];
+    int sp = 0;
+    int32_t cur = 0, row = 0, idx = 0;
+    while (true) {
+        const bool idle = qi < 0 && !exhausted;
+        const uint32_t need = __ballot_sync(0xffffffffu, idle);
+        const uint32_t busy = __ballot_sync(0xffffffffu, qi >= 0);
+        if (need && (__popc(need) >= 8 || busy == 0)) {
+            const int leader = __ffs(need) - 1;
+            int32_t base = 0;
+            if ((int)lane == leader) base = atomicAdd(fetch, __popc(need));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (idle) {
+                const int32_t my = base + __popc(need & ((1u << lane) - 1u));
+                if (my < n) {
+                    const QRay q = m.shq[my];
+                    o = mk(q.ox, q.oy, q.oz);
+                    d = mk(q.dx, q.dy, q.dz);
+                    tmax = q.tmax;
+                    row = q.row;
+                    idx = q.idx;
+                    r32 = bvh::prep32(o, d);
+                    t0 = bvh::t_lo32(t_min);
+                    t1 = bvh::t_hi32(tmax);
+                    sp = 0;
+                    cur = 0;
+                    qi = my;
+                } else {
+                    exhausted = true;
+                }
+            }
+        }
+        if (__all_sync(0xffffffffu, exhausted || qi < 0) && __all_sync(0xffffffffu, exhausted)) break;
+        if (qi < 0) continue;
+        // one node of the traversal (bvh::any_hit_w, unrolled into steps)
+        const WNode w = bvh::load_w(b.wnodes, cur);
+        bool h0, h1;
+        float n0, n1;
+        bvh::wchildren(w, r32, t0, t1, h0, h1, n0, n1);
+        bool blocked = false;
+        if (h0 && w.r.x < 0) { blocked = bvh::leaf_any(b, w.r.x, o, d, t_min, tmax); h0 = false; }
+        if (!blocked && h1 && w.r.y < 0) {
+            blocked = bvh::leaf_any(b, w.r.y, o, d, t_min, tmax);
+            h1 = false;
+        }
+        bool done = blocked;
+        if (!done) {
+            if (h0 && h1) {
+                if (sp < bvh::kStack) stack[sp++] = w.r.y;
+                cur = w.r.x;
+            } else if (h0 || h1) {
+                cur = h0 ? w.r.x : w.r.y;
+            } else if (sp > 0) {
+                cur = stack[--sp];
+            } else {
+                done = true;
+            }
+        }
+        if (done) {
+            m.shadow[row] = blocked ? idx + 1 : 0;
+            qi = -1;
+        }
+    }
 }
 
 // Device-driven march round (no host sync): flip to the queue k_step will
@@ -562,6 +669,8 @@ __global__ void k_round_begin(int32_t* c, unsigned long long* stats, int32_t tar
     c[C_STRIDE] = live;
     c[C_MQ0 + (cur ^ 1)] = 0;
     c[C_NS] = 0;
+    c[C_SHQ] = 0;
+    c[C_SHF] = 0;
     (void)stats;
 }
 
@@ -576,6 +685,8 @@ __global__ void k_march_begin(int32_t* c) {
 // Start of a march round: empty the batch and the next march queue.
 __global__ void k_round_reset(int32_t* counters, int32_t next_mq) {
     counters[C_NS] = 0;
+    counters[C_SHQ] = 0;
+    counters[C_SHF] = 0;
     counters[C_MQ0 + next_mq] = 0;
 }
 

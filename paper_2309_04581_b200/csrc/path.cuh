@@ -93,13 +93,20 @@ HRT_DEV double dense_sample(const DevField& f, d3 p, double rgb[3]) {
 // ----------------------------------------------------------------- shadows
 // EmitterSet.sample + shadow_mask_batch (render.py:96-123) for one point:
 // 0 if the sampled emitter point is visible, else 1 + emitter index.
-HRT_DEV int32_t shadow_code(const DevScene& sc, d3 p, uint64_t seed, int64_t pix, int64_t smp,
-                            int64_t bounce, int64_t lane) {
+struct ShadowRay {          // one shadow query: point p towards emitter idx, interval (eps, tmax]
+    d3 dir;
+    double tmax;
+    int32_t idx;
+};
+
+// EmitterSet.sample (render.py:96-107) + the ray set-up of shadow_mask_batch
+// (render.py:110-123) for one point.
+// h4 = rng::prefix(seed, pix, smp, bounce) of the path segment.
+HRT_DEV ShadowRay shadow_ray_h(const DevScene& sc, d3 p, uint64_t h4, int64_t lane) {
     const DevEmitters& em = sc.em;
-    if (em.n == 0) return 0;
-    const double u_pick = rng::uniform(seed, pix, smp, bounce, rng::LIGHT_PICK, lane);
-    const double u1 = rng::uniform(seed, pix, smp, bounce, rng::LIGHT_U, lane);
-    const double u2 = rng::uniform(seed, pix, smp, bounce, rng::LIGHT_V, lane);
+    const double u_pick = rng::uniform_from(h4, rng::LIGHT_PICK, lane);
+    const double u1 = rng::uniform_from(h4, rng::LIGHT_U, lane);
+    const double u2 = rng::uniform_from(h4, rng::LIGHT_V, lane);
     int lo = 0, hi = em.n;            // searchsorted(cdf, u, 'right')
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
@@ -114,9 +121,25 @@ HRT_DEV int32_t shadow_code(const DevScene& sc, d3 p, uint64_t seed, int64_t pix
     const d3 delta = sub(q, p);
     const double dist = norm(delta);
     const double safe = fmax(dist, 1e-12);
-    const d3 dir = {delta.x / safe, delta.y / safe, delta.z / safe};
-    const bool blocked = bvh::occluded(sc.blockers, p, dir, sc.spawn_eps, dist * (1.0 - 1e-4));
-    return blocked ? idx + 1 : 0;
+    ShadowRay r;
+    r.dir = {delta.x / safe, delta.y / safe, delta.z / safe};
+    r.tmax = dist * (1.0 - 1e-4);
+    r.idx = idx;
+    return r;
+}
+
+HRT_DEV ShadowRay shadow_ray(const DevScene& sc, d3 p, uint64_t seed, int64_t pix, int64_t smp,
+                             int64_t bounce, int64_t lane) {
+    return shadow_ray_h(sc, p, rng::prefix(seed, pix, smp, bounce), lane);
+}
+
+// 0 if the sampled emitter point is visible from p, else 1 + emitter index.
+HRT_DEV int32_t shadow_code(const DevScene& sc, d3 p, uint64_t seed, int64_t pix, int64_t smp,
+                            int64_t bounce, int64_t lane) {
+    if (sc.em.n == 0) return 0;
+    const ShadowRay r = shadow_ray(sc, p, seed, pix, smp, bounce, lane);
+    const bool blocked = bvh::occluded(sc.blockers, p, r.dir, sc.spawn_eps, r.tmax);
+    return blocked ? r.idx + 1 : 0;
 }
 
 // Mask value of a shadow code: 1, or clip(1 - r_src, 0.02, 1) when blocked.
