@@ -162,10 +162,26 @@ def _cpu_tile(args):
     return st["nerf_samples"], st["paths"]
 
 
-def cpu_sample(n_tiles, workers, cam_index=0, seed=0):
+def cpu_pool(workers):
+    """One forked worker per core, created once (scene inherited, imports
+    warmed by a tiny job) so timed samples measure tracing, not start-up."""
+    import multiprocessing as mp
+    _cpu_scene()
+    pool = mp.get_context("fork").Pool(workers)
+    pool.map(_warm, range(workers))
+    return pool
+
+
+def _warm(_):
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+    from oracle import tracer  # noqa: F401
+    return 0
+
+
+def cpu_sample(n_tiles, workers, cam_index=0, seed=0, pool=None):
     """Oracle (numpy port of the reference path) on `n_tiles` seeded 16x16
     tiles of the cfg1 frame, one process per core."""
-    import multiprocessing as mp
     import numpy as np
     rng = np.random.default_rng(seed)
     all_t = (800 // TILE) * (800 // TILE)
@@ -175,12 +191,15 @@ def cpu_sample(n_tiles, workers, cam_index=0, seed=0):
         x0, y0 = (t % (800 // TILE)) * TILE, (t // (800 // TILE)) * TILE
         ys, xs = np.meshgrid(np.arange(y0, y0 + TILE), np.arange(x0, x0 + TILE), indexing="ij")
         jobs.append((cam_index, (ys * 800 + xs).reshape(-1)))
-    _cpu_scene()
-    ctx = mp.get_context("fork")
+    own = pool is None
+    if own:
+        pool = cpu_pool(workers)
     t0 = time.perf_counter()
-    with ctx.Pool(workers) as pool:
-        res = pool.map(_cpu_tile, jobs, chunksize=1)
+    res = pool.map(_cpu_tile, jobs, chunksize=1)
     dt = time.perf_counter() - t0
+    if own:
+        pool.close()
+        pool.join()
     samples = sum(r[0] for r in res)
     paths = sum(r[1] for r in res)
     return samples, paths, dt
@@ -196,8 +215,10 @@ def cpu_workers():
 def cpu_baseline_block(n_tiles=0):
     workers = cpu_workers()
     n_tiles = n_tiles or max(16, 8 * workers)
-    # warm the worker imports once with a tiny job so the timed sample is steady-state
-    samples, paths, dt = cpu_sample(n_tiles, workers)
+    pool = cpu_pool(workers)             # forked + warmed before the timed sample
+    samples, paths, dt = cpu_sample(n_tiles, workers, pool=pool)
+    pool.close()
+    pool.join()
     return {"value": samples / dt, "unit": "samples/s", "cores": workers, "kind": "port",
             "mrays_per_s": paths / dt / 1e6,
             "sample": f"{n_tiles} seeded 16x16 tiles ({paths} paths, {samples} NeRF samples) of the "
@@ -211,13 +232,16 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     workers = cpu_workers()
-    n_tiles = args.cpu_tiles or max(8, 2 * workers)
+    n_tiles = args.cpu_tiles or max(8, 4 * workers)
+    pool = cpu_pool(workers)
     for _ in range(max(0, min(args.warmup, 1))):
-        cpu_sample(max(1, workers), workers)
+        cpu_sample(max(1, workers), workers, pool=pool)
     tot_s = tot_p = tot_t = 0.0
     for k in range(args.steps):
-        s, p, dt = cpu_sample(n_tiles, workers, cam_index=k % 100, seed=k)
+        s, p, dt = cpu_sample(n_tiles, workers, cam_index=k % 100, seed=k, pool=pool)
         tot_s, tot_p, tot_t = tot_s + s, tot_p + p, tot_t + dt
+    pool.close()
+    pool.join()
     value = tot_s / tot_t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
@@ -229,7 +253,7 @@ def run_reference(args, rank, world):
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": workers, "kind": "port",
                          "sample": f"{n_tiles} seeded 16x16 tiles per step x {args.steps} steps, "
                                    f"oracle/ numpy port of the reference render loop + neural "
-                                   f"field, one process per core"},
+                                   f"field, one process per core (pool forked and warmed once)"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
