@@ -170,10 +170,25 @@ int hrt_trace_paths(hrt_handle* h, const double* o, const double* d, const int64
                     const int64_t* sample, int64_t n, uint64_t seed, int32_t mode, double* L,
                     void* stream);
 
+/* Transport operator of emitter estimation (emitters.py:73-166,
+ * build_transport): per pose, surface-only paths (n_bounces = max_depth, no
+ * field) whose front-facing hits add T_spec / spp to
+ * A[pose*w*h + pixel, face, :] instead of multiplying the face emission, so
+ * image = A @ emission. out: device float64 (n_poses*w*h, n_faces, 3),
+ * zeroed by the call; sums in the reference's np.add.at order. */
+int hrt_transport(hrt_handle* h, const hrt_camera* cams, int32_t n_poses, int32_t spp, uint64_t seed,
+                  int32_t max_depth, double* out, void* stream);
+
 /* Debug trace of evaluated NeRF samples: int32 records (path, bounce, k,
  * occupancy cell) in device memory, up to cap records; enabled for the
  * next hrt_render call only. */
 int hrt_set_trace(hrt_handle* h, int32_t* records, int64_t cap);
+
+/* RenderConfig of later calls (scene.py:138-144 + spawn_eps, sample cap,
+ * early-out): the reference reads scene.render at every render, so a changed
+ * config applies without re-uploading the scene. */
+int hrt_set_config(hrt_handle* h, int32_t n_bounces, double threshold, double march_step,
+                   double spawn_eps, int32_t sample_cap, double early_t);
 
 /* Per-stage device timing of later hrt_render calls into hrt_stats.stage_ms
  * (on != 0) or off (default). Measurement aid: adds one event pair per launch. */

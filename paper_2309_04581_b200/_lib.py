@@ -103,8 +103,12 @@ SIGNATURES = {
                                        ctypes.c_int32, vp, vp]),
     "hrt_set_trace": (ctypes.c_int, [vp, vp, ctypes.c_int64]),
     "hrt_set_profile": (ctypes.c_int, [vp, ctypes.c_int32]),
+    "hrt_set_config": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_int32, ctypes.c_double]),
     "hrt_finalize": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, vp, vp, ctypes.c_int64, ctypes.c_int32,
                                     vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64), vp]),
+    "hrt_transport": (ctypes.c_int, [vp, vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64,
+                                     ctypes.c_int32, vp, vp]),
     "hrt_gather_peak": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
     "hrt_refit": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "hrt_field_sample": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, vp]),

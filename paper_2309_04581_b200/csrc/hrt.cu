@@ -851,6 +851,21 @@ int hrt_set_trace(hrt_handle* h, int32_t* records, int64_t cap) {
     return HRT_OK;
 }
 
+int hrt_set_config(hrt_handle* h, int32_t n_bounces, double threshold, double march_step,
+                   double spawn_eps, int32_t sample_cap, double early_t) {
+    if (!h) return fail(HRT_EINVAL, "null handle");
+    if (!(march_step > 0)) return fail(HRT_EINVAL, "march step must be > 0");
+    if (n_bounces < 0) return fail(HRT_EINVAL, "n_bounces must be >= 0");
+    DevScene& sc = h->sc;
+    sc.n_bounces = n_bounces;
+    sc.threshold = threshold;
+    sc.march_step = march_step;
+    sc.spawn_eps = spawn_eps;
+    sc.sample_cap = sample_cap;
+    sc.early_t = early_t;
+    return HRT_OK;
+}
+
 int hrt_set_profile(hrt_handle* h, int32_t on) {
     if (!h) return fail(HRT_EINVAL, "null handle");
     if (on && h->pev.empty()) {
@@ -944,6 +959,66 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
     }
     if (ctr[C_NONFINITE] != 0) return fail(HRT_ENONFINITE, "non-finite or negative radiance in frame");
     return HRT_OK;
+}
+
+int hrt_transport(hrt_handle* h, const hrt_camera* cams, int32_t n_poses, int32_t spp, uint64_t seed,
+                  int32_t max_depth, double* out, void* stream) {
+    if (!h || !cams || !out) return fail(HRT_EINVAL, "null argument");
+    if (n_poses < 1 || spp < 1 || max_depth < 1) return fail(HRT_EINVAL, "n_poses, spp, max_depth must be >= 1");
+    if (h->sc.field.kind != HRT_FIELD_NONE) return fail(HRT_EINVAL, "estimation scenes must not contain a radiance field");
+    const int32_t w = cams[0].width, hh = cams[0].height;
+    for (int i = 0; i < n_poses; ++i)
+        if (cams[i].width != w || cams[i].height != hh) return fail(HRT_EINVAL, "all poses must share one resolution");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t npix = (int64_t)w * hh;
+    const int32_t F = h->bvh.n_faces;
+    const int32_t per_batch = (int32_t)std::max<int64_t>(1, 65536 / npix);   // emitters.py:151
+    CK(cudaMemsetAsync(out, 0, (size_t)n_poses * npix * F * 3 * sizeof(double), st));
+    const int64_t chunk_pix = std::max<int64_t>(1, kMaxPaths / spp);
+    int rc;
+    if ((rc = ensure_state(h, std::min<int64_t>(npix, chunk_pix) * spp))) return rc;
+    const int64_t nrec = std::min<int64_t>(npix, chunk_pix) * spp * max_depth;
+    int32_t* rface = nullptr;
+    double* rval = nullptr;
+    CK(cudaMallocAsync(&rface, (size_t)nrec * 4, st));
+    CK(cudaMallocAsync(&rval, (size_t)nrec * 24, st));
+    DevScene sc = h->sc;
+    sc.n_bounces = max_depth;                     // emitters.py:140 (temporary n_bounces)
+    for (int pose = 0; pose < n_poses && rc == HRT_OK; ++pose) {
+        for (int64_t p0 = 0; p0 < npix; p0 += chunk_pix) {
+            const int64_t np = std::min(chunk_pix, npix - p0), paths = np * spp;
+            kern::Args a{};
+            a.sc = sc;
+            a.ps = h->ps;
+            a.cam = to_cam(cams[pose]);
+            a.pixel_base = p0;
+            a.n_slots = np;
+            a.spp = spp;
+            a.strat = strat_of(spp);
+            a.seed = seed;
+            a.tiled = 0;
+            CK(cudaMemsetAsync(rface, 0xff, (size_t)paths * max_depth * 4, st));
+            CK(cudaMemsetAsync(h->ps.counters, 0, 64 * 4, st));
+            kern::k_raygen<<<grid_for(h, paths), kThreads, 0, st>>>(a);
+            CK(cudaGetLastError());
+            const unsigned g = grid_for(h, paths);
+            for (int b = 1; b <= max_depth; ++b) {
+                a.bounce = b;
+                a.cur = (b - 1) & 1;
+                kern::k_reset_queue<<<1, 1, 0, st>>>(h->ps.counters, a.cur ^ 1);
+                kern::k_intersect<<<g, kThreads, 0, st>>>(a);
+                kern::k_shade_transport<<<g, kThreads, 0, st>>>(a, max_depth, rface, rval);
+                CK(cudaGetLastError());
+            }
+            kern::k_transport_reduce<<<grid_for(h, np), kThreads, 0, st>>>(
+                np, spp, max_depth, per_batch, F, rface, rval, (int64_t)pose * npix + p0, out);
+            CK(cudaGetLastError());
+        }
+    }
+    CK(cudaFreeAsync(rface, st));
+    CK(cudaFreeAsync(rval, st));
+    CK(cudaStreamSynchronize(st));
+    return rc;
 }
 
 int hrt_trace_paths(hrt_handle* h, const double* o, const double* d, const int64_t* pixel,

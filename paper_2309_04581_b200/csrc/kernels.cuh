@@ -482,7 +482,10 @@ __global__ void __launch_bounds__(256, HRT_COMP_MINB) k_comp(Args a, MarchState 
 // generates its next samples at rows i * nq + r. One pass over the path
 // state per round instead of two (k_gen + k_comp); a path whose remaining
 // candidates are all empty cells keeps a rank with S hole rows.
-__global__ void __launch_bounds__(256, 1) k_step(Args a, MarchState m) {
+#ifndef HRT_STEP_MINB
+#define HRT_STEP_MINB 3
+#endif
+__global__ void __launch_bounds__(256, HRT_STEP_MINB) k_step(Args a, MarchState m) {
     const int32_t* ctr = a.ps.counters;
     const int32_t mcur = ctr[C_CUR], S = ctr[C_S], prev_nq = ctr[C_PSTRIDE], first = ctr[C_FIRST];
     const int32_t nq = ctr[C_MQ0 + mcur];
@@ -737,6 +740,84 @@ __global__ void k_shade(Args a) {
         s.dx[p] = nd.x; s.dy[p] = nd.y; s.dz[p] = nd.z;
         store_acc(s, p, c);
         if (fmax(fmax(c.Ts[0], c.Ts[1]), c.Ts[2]) >= sc.threshold) next[reserve(next_n)] = p;
+    }
+}
+
+// ---------------------------------------------- emitter-estimation transport
+// _trace_transport (emitters.py:73-111): like k_shade, but a front-facing hit
+// records (face, T_spec / spp) for its bounce instead of adding the face's
+// emission; k_transport_reduce adds the records into A in the reference's
+// np.add.at order.
+__global__ void k_shade_transport(Args a, int32_t depth, int32_t* rec_face, double* rec_val) {
+    const int32_t n = a.ps.counters[a.cur];
+    const int32_t* q = pick(a.ps.queue, a.cur);
+    int32_t* next = pick(a.ps.queue, a.cur ^ 1);
+    int32_t* next_n = &a.ps.counters[a.cur ^ 1];
+    const PathState& s = a.ps;
+    const DevScene& sc = a.sc;
+    const double inv_spp = 1.0 / (double)a.spp;
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const int32_t p = q[j];
+        const int32_t f = s.face[p];
+        if (f < 0) continue;
+        const double t = s.t_hit[p];
+        const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+        const d3 point = {o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
+        const d3 n_raw = mk(sc.normal[3 * f], sc.normal[3 * f + 1], sc.normal[3 * f + 2]);
+        const bool facing = dot(n_raw, d) < 0.0;
+        const d3 nrm = facing ? n_raw : neg(n_raw);
+        double T[3] = {s.Tr[p], s.Tg[p], s.Tb[p]};
+        if (facing) {
+            const int64_t r = (int64_t)p * depth + (a.bounce - 1);
+            rec_face[r] = f;
+            for (int ch = 0; ch < 3; ++ch) rec_val[3 * r + ch] = T[ch] * inv_spp;
+        }
+        const int32_t mi = sc.mesh_of[f];
+        const int32_t kind = sc.mat.kind[mi];
+        const d3 wo = neg(d);
+        const int32_t pix = s.pix[p], smp = s.smp[p];
+        d3 nd;
+        if (kind == 0) {
+            const double u1 = rng::uniform(a.seed, pix, smp, a.bounce, rng::BSDF_U, 0);
+            const double u2 = rng::uniform(a.seed, pix, smp, a.bounce, rng::BSDF_V, 0);
+            nd = path::cosine_sample(nrm, u1, u2);
+        } else if (kind == 1) {
+            nd = path::reflect(wo, nrm);
+        } else {
+            const double u = rng::uniform(a.seed, pix, smp, a.bounce, rng::BSDF_LOBE, 0);
+            nd = path::dielectric_sample(wo, nrm, facing, sc.mat.ior[mi], sc.mat.r0[mi], u);
+        }
+        for (int ch = 0; ch < 3; ++ch) T[ch] = T[ch] * sc.mat.rgb[3 * mi + ch];
+        s.Tr[p] = T[0]; s.Tg[p] = T[1]; s.Tb[p] = T[2];
+        s.ox[p] = point.x + sc.spawn_eps * nd.x;
+        s.oy[p] = point.y + sc.spawn_eps * nd.y;
+        s.oz[p] = point.z + sc.spawn_eps * nd.z;
+        s.dx[p] = nd.x; s.dy[p] = nd.y; s.dz[p] = nd.z;
+        if (fmax(fmax(T[0], T[1]), T[2]) >= sc.threshold) next[reserve(next_n)] = p;
+    }
+}
+
+// One thread per pixel of the chunk: A[row0 + pixel, face, :] += records in
+// the reference's order (emitters.py:147-159 batches of `per_batch` samples
+// of every pixel; per batch bounce 1..depth, samples in order; np.add.at is
+// sequential). Paths of slot i are i * spp + s (k_raygen).
+__global__ void k_transport_reduce(int64_t n_slots, int32_t spp, int32_t depth, int32_t per_batch,
+                                   int32_t n_faces, const int32_t* __restrict__ rec_face,
+                                   const double* __restrict__ rec_val, int64_t pixel_base,
+                                   double* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_slots;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double* row = out + (pixel_base + i) * (int64_t)n_faces * 3;
+        for (int32_t s0 = 0; s0 < spp; s0 += per_batch) {
+            const int32_t s1 = min(spp, s0 + per_batch);
+            for (int32_t b = 0; b < depth; ++b)
+                for (int32_t smp = s0; smp < s1; ++smp) {
+                    const int64_t r = (i * spp + smp) * depth + b;
+                    const int32_t f = rec_face[r];
+                    if (f < 0) continue;
+                    for (int ch = 0; ch < 3; ++ch) row[3 * f + ch] = row[3 * f + ch] + rec_val[3 * r + ch];
+                }
+        }
     }
 }
 

@@ -45,6 +45,13 @@ class Renderer:
         self.handle = handle
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.last_stats = {}
+        self.config = _config_of(self.pack)
+
+    def set_config(self, config):
+        """(n_bounces, threshold, march_step, spawn_eps, sample_cap, early_t) for later renders."""
+        if tuple(config) != self.config:
+            _lib.check(self.lib.hrt_set_config(self.handle, *config), "hrt_set_config")
+            self.config = tuple(config)
 
     def close(self):
         if getattr(self, "handle", None):
@@ -197,7 +204,21 @@ def _geometry_key(scene):
     return getattr(scene, "version", None), id(getattr(scene, "bvh", None))
 
 
+def _config_of(pack):
+    return (int(pack["n_bounces"]), float(pack["threshold"]), float(pack["march_step"]),
+            float(pack["spawn_eps"]), int(pack["sample_cap"]), float(pack["early_t"]))
+
+
+def _scene_config(scene, spawn_eps):
+    rc = scene.render
+    return (int(rc.n_bounces), float(rc.threshold), float(rc.march_step), float(spawn_eps),
+            int(getattr(rc, "sample_cap", 0) or 0), float(getattr(rc, "early_t", 0.0) or 0.0))
+
+
 def renderer_for(scene) -> Renderer:
+    """The scene's cached renderer: geometry changes refit, RenderConfig
+    changes (read at every call, as the reference does) are pushed with
+    hrt_set_config."""
     cached = getattr(scene, "_hrt_renderer", None)
     key = _geometry_key(scene)
     dev = torch.cuda.current_device()
@@ -206,9 +227,10 @@ def renderer_for(scene) -> Renderer:
         if cached[0] != key:
             r.refit(scene)
             scene._hrt_renderer = (key, r, dev)
-        return r
-    r = Renderer(scene)
-    scene._hrt_renderer = (key, r, dev)
+    else:
+        r = Renderer(scene)
+        scene._hrt_renderer = (key, r, dev)
+    r.set_config(_scene_config(scene, r.pack["spawn_eps"]))
     return r
 
 

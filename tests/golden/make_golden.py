@@ -11,6 +11,8 @@ pin both the CPU oracle (tests/test_golden.py, not gpu) and the CUDA path
   field.npz   RadianceGrid.sample_batch incl. outside / borders  (field.py:143-161)
   images.npz  finalize -> encode_ppm / encode_pfm bytes of 3 HDR frames incl. the sRGB
               cut, the 1.0 rail, > 1, zeros and tiny values   (render.py:399-401, images.py:37-64)
+  transport.npz  emitters.build_transport (per-face transport operator) of a Lambertian
+              room with an emissive quad, 2 poses, 4 spp, max_depth 3  (emitters.py:73-166)
   render.npz  render / render_surface_only / render_volume_only on dense-grid scenes
               (mirror fog, glass fog, Lambertian room, shadowed slab), with every
               input array needed to rebuild the scenes without the reference.
@@ -30,6 +32,7 @@ from hybridrt.core import Transform  # noqa: E402
 from hybridrt.field import RadianceGrid  # noqa: E402
 from hybridrt.images import HdrImage  # noqa: E402
 from hybridrt.render import finalize  # noqa: E402
+from hybridrt.emitters import build_transport  # noqa: E402
 from hybridrt.render import (Camera, EmitterSet, _sample_jitter, render,  # noqa: E402
                              render_surface_only, render_volume_only)
 from hybridrt.scene import CameraConfig, RenderConfig, Scene, SceneConfig, scene_diagonal  # noqa: E402
@@ -129,6 +132,21 @@ def gen_images():
         out[f"pfm{i}"] = np.frombuffer(finalize(img, True), np.uint8)
     np.savez_compressed(os.path.join(OUT, "images.npz"), **out)
 
+
+def gen_transport():
+    bv, bf = assets.box((-2, -2, -2), (2, 2, 2), inward=True)
+    qv, qf = assets.quad((-1, -1, -1.9), (2, 0, 0), (0, 2, 0))
+    cv, cf = assets.box((-0.5, -1.5, -1.0), (0.3, -0.4, 0.2))
+    room = [TriangleMesh(bv, bf, Lambertian(np.full(3, 0.6))),
+            TriangleMesh(qv, qf, Lambertian(np.array((0.2, 0.3, 0.4))), emission=np.array((3.0, 2.0, 1.0))),
+            TriangleMesh(cv, cf, Lambertian(np.array((0.7, 0.5, 0.3))))]
+    poses = [Camera(Transform.look_at([0, 0, 1.5], [0, 0, -1]), math.radians(60), (12, 10)),
+             Camera(Transform.look_at([1.2, 0.8, 1.0], [0, -0.5, -1]), math.radians(50), (12, 10))]
+    sc = make_scene(meshes=room, camera=poses[0], spp=4, seed=9, n_bounces=8)
+    op = build_transport(sc, poses, max_depth=3)
+    np.savez_compressed(os.path.join(OUT, "transport.npz"), a=op.a, bv=bv, bf=bf, qv=qv, qf=qf,
+                        cv=cv, cf=cf)
+
 def gen_render():
     out = {}
     v, f = assets.icosphere(0.4, 2)
@@ -179,6 +197,7 @@ if __name__ == "__main__":
     gen_bvh()
     gen_field()
     gen_images()
+    gen_transport()
     gen_render()
     for fn in sorted(os.listdir(OUT)):
         if fn.endswith(".npz"):
