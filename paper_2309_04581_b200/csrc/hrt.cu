@@ -9,6 +9,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/hrt.h"
@@ -36,6 +37,7 @@ int fail(int code, const std::string& msg) {
 constexpr int64_t kMaxPaths = int64_t(1) << 20;   // paths per wavefront chunk
 constexpr int kThreads = 256;
 constexpr int kTimedLaunches = 1024;
+constexpr int kIoChunks = 4;                       // pieces of the e2e frame read-back
 #ifndef HRT_SHADOW_QUEUE
 #define HRT_SHADOW_QUEUE 1
 #endif
@@ -91,6 +93,7 @@ struct hrt_handle {
     int32_t *io_pix = nullptr, *io_pix_host = nullptr;
     double *io_out = nullptr, *io_out_host = nullptr;
     cudaStream_t io_stream = nullptr;
+    cudaEvent_t io_ev[8] = {};
     int n_timed = 0;
     int64_t launches = 0;
     uint32_t* occ_dev = nullptr;
@@ -134,6 +137,7 @@ struct hrt_handle {
         if (io_pix_host) cudaFreeHost(io_pix_host);
         if (io_out_host) cudaFreeHost(io_out_host);
         if (io_stream) cudaStreamDestroy(io_stream);
+        for (cudaEvent_t e : io_ev) if (e) cudaEventDestroy(e);
         if (tex) cudaDestroyTextureObject(tex);
     }
 };
@@ -540,8 +544,27 @@ int ensure_io(hrt_handle* h, int64_t npx) {
     CK(cudaMallocHost(&h->io_pix_host, n * 4));
     CK(cudaMallocHost(&h->io_out_host, n * 24));
     if (!h->io_stream) CK(cudaStreamCreateWithFlags(&h->io_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : h->io_ev)
+        if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     h->io_cap = npx;
     return HRT_OK;
+}
+
+// memcpy split over a few host threads (one core copies ~10 GB/s; the frame
+// read-back of the e2e path is 15 MB at 800x800).
+void par_copy(char* dst, const char* src, size_t len) {
+    constexpr size_t kMin = size_t(1) << 20;
+    const int nt = (int)std::min<size_t>(4, std::max<size_t>(1, len / kMin));
+    if (nt == 1) { std::memcpy(dst, src, len); return; }
+    std::vector<std::thread> ts;
+    const size_t part = (len + nt - 1) / nt;
+    for (int t = 1; t < nt; ++t) {
+        const size_t off = t * part;
+        if (off >= len) break;
+        ts.emplace_back([=] { std::memcpy(dst + off, src + off, std::min(part, len - off)); });
+    }
+    std::memcpy(dst, src, std::min(part, len));
+    for (auto& t : ts) t.join();
 }
 
 int read_counter(hrt_handle* h, int idx, cudaStream_t st, int32_t* v) {
@@ -1059,14 +1082,27 @@ int hrt_render_host(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t 
     if ((rc = ensure_io(h, npx))) return rc;
     cudaStream_t st = h->io_stream;
     if (pixels) {       // stage through pinned memory so the H2D is a true async DMA
-        std::memcpy(h->io_pix_host, pixels, (size_t)npx * 4);
+        par_copy(reinterpret_cast<char*>(h->io_pix_host), reinterpret_cast<const char*>(pixels), (size_t)npx * 4);
         CK(cudaMemcpyAsync(h->io_pix, h->io_pix_host, (size_t)npx * 4, cudaMemcpyHostToDevice, st));
     }
     rc = hrt_render(h, cam, spp, seed, mode, pixels ? h->io_pix : nullptr, npx, h->io_out, stats, st);
     if (rc == HRT_OK || rc == HRT_ENONFINITE) {
-        CK(cudaMemcpyAsync(h->io_out_host, h->io_out, (size_t)npx * 24, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        std::memcpy(out, h->io_out_host, (size_t)npx * 24);
+        // frame back in kIoChunks DMA pieces; the pinned -> caller copy of piece k
+        // (split over host threads) overlaps the DMA of pieces k+1..
+        const size_t bytes = (size_t)npx * 24;
+        const size_t piece = (bytes / kIoChunks + 4095) & ~size_t(4095);
+        int nk = 0;
+        for (size_t off = 0; off < bytes; off += piece, ++nk) {
+            const size_t len = std::min(piece, bytes - off);
+            CK(cudaMemcpyAsync(reinterpret_cast<char*>(h->io_out_host) + off,
+                               reinterpret_cast<const char*>(h->io_out) + off, len, cudaMemcpyDeviceToHost, st));
+            CK(cudaEventRecord(h->io_ev[nk], st));
+        }
+        for (int k = 0; k < nk; ++k) {
+            CK(cudaEventSynchronize(h->io_ev[k]));
+            const size_t off = (size_t)k * piece, len = std::min(piece, bytes - off);
+            par_copy(reinterpret_cast<char*>(out) + off, reinterpret_cast<const char*>(h->io_out_host) + off, len);
+        }
     }
     return rc;
 }
