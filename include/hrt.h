@@ -184,6 +184,15 @@ int hrt_transport(hrt_handle* h, const hrt_camera* cams, int32_t n_poses, int32_
  * next hrt_render call only. */
 int hrt_set_trace(hrt_handle* h, int32_t* records, int64_t cap);
 
+/* Rigid per-mesh motion refit on the device (cfg3: 200 meshes move each
+ * frame; sim.py:673-698 sync_to_renderer -> scene.py:475-479 rebuild).
+ * set_rigid_base: object-space corners (n_faces x 9: p0, p1, p2) in global
+ * face order, and the global face id of every blocker face. refit_rigid:
+ * n_meshes row-major 3x4 world_from_object matrices; world faces, normals
+ * and both trees are rebuilt / refit on the GPU (no per-frame face upload). */
+int hrt_set_rigid_base(hrt_handle* h, const double* corners, const int32_t* blocker_faces);
+int hrt_refit_rigid(hrt_handle* h, const double* xf, int32_t n_meshes);
+
 /* RenderConfig of later calls (scene.py:138-144 + spawn_eps, sample cap,
  * early-out): the reference reads scene.render at every render, so a changed
  * config applies without re-uploading the scene. */

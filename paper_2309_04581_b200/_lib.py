@@ -109,6 +109,8 @@ SIGNATURES = {
                                     vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64), vp]),
     "hrt_transport": (ctypes.c_int, [vp, vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64,
                                      ctypes.c_int32, vp, vp]),
+    "hrt_set_rigid_base": (ctypes.c_int, [vp, vp, vp]),
+    "hrt_refit_rigid": (ctypes.c_int, [vp, vp, ctypes.c_int32]),
     "hrt_gather_peak": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
     "hrt_refit": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "hrt_field_sample": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, vp]),

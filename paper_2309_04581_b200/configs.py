@@ -104,14 +104,33 @@ def cfg3_layout(seed=3, n=200):
     return radii, centres, kinds, velocity
 
 
+def apply_rigid(v, m):
+    """World points of object points v (n, 3) under a 3x4 world_from_object m,
+    row r as ((m0*x + m1*y) + m2*z) + m3 - the order hrt_refit_rigid uses."""
+    v = np.asarray(v, np.float64)
+    return np.stack([((m[r, 0] * v[:, 0] + m[r, 1] * v[:, 1]) + m[r, 2] * v[:, 2]) + m[r, 3]
+                     for r in range(3)], axis=1)
+
+
+def cfg3_transforms(frame, layout=None):
+    """(200, 3, 4) world_from_object of every sphere at `frame` (P11: scale by
+    the radius, translate to centre + frame * velocity)."""
+    radii, centres, _, vel = layout or cfg3_layout()
+    xf = np.zeros((len(radii), 3, 4))
+    for a in range(3):
+        xf[:, a, a] = radii
+    xf[:, :, 3] = centres + frame * vel
+    return xf
+
+
 def cfg3(field=None, frame=0, res=(1920, 1080)):
     radii, centres, kinds, vel = cfg3_layout()
     base_v, base_f = assets.icosphere(1.0, 4)
+    xf = cfg3_transforms(frame)
     meshes = []
     for i in range(len(radii)):
-        c = centres[i] + frame * vel[i]
         bsdf = (Mirror(np.full(3, 0.9)), Dielectric(1.5), Lambertian(np.full(3, 0.7)))[kinds[i]]
-        meshes.append(TriangleMesh(base_v * radii[i] + c, base_f, bsdf, name=f"ico{i}"))
+        meshes.append(TriangleMesh(apply_rigid(base_v, xf[i]), base_f, bsdf, name=f"ico{i}"))
     cam = Camera(look_at_safe((0.0, 0.4, 4.5)), math.radians(40.0), res)
     return Scene(camera=cam, render=_march(spp=8, n_bounces=4, threshold=1e-4, sample_cap=1024,
                                            early_t=1e-4),
@@ -119,11 +138,13 @@ def cfg3(field=None, frame=0, res=(1920, 1080)):
 
 
 def cfg3_move(scene, frame):
-    """Rigid motion of frame `frame` applied in place (then renderer refits)."""
-    radii, centres, kinds, vel = cfg3_layout()
+    """Rigid motion of frame `frame` applied in place on the host (the
+    renderer then refits from the world faces; hrt_refit_rigid does the same
+    from cfg3_transforms without touching the host meshes)."""
     base_v, _ = assets.icosphere(1.0, 4)
+    xf = cfg3_transforms(frame)
     for i, m in enumerate(scene.meshes):
-        m.vertices = base_v * radii[i] + centres[i] + frame * vel[i]
+        m.vertices = apply_rigid(base_v, xf[i])
         m.recompute_normals()
     scene.touch()
 

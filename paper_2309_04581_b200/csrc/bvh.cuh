@@ -327,8 +327,8 @@ HRT_DEV void wbox_dev(const BvhNode& n, float lo[3], float hi[3]) {
 }
 
 __global__ void k_wsync(WNode* w, const int2* __restrict__ src, const BvhNode* __restrict__ nodes,
-                        int32_t n) {
-    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+                        int32_t begin, int32_t n) {
+    for (int32_t i = begin + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int2 sidx = src[i];
         float l0[3], h0[3], l1[3], h1[3];
         if (sidx.x >= 0) wbox_dev(nodes[sidx.x], l0, h0);
@@ -402,6 +402,66 @@ __global__ void k_refit(BvhNode* nodes, const int32_t* __restrict__ parent,
             }
             node = p;
         }
+    }
+}
+
+
+// Root boxes of a forest's trees (6 doubles each) for the host top-level build.
+__global__ void k_root_boxes(const BvhNode* __restrict__ nodes, const int32_t* __restrict__ roots, int32_t g,
+                             double* out) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g) return;
+    const BvhNode& n = nodes[roots[i]];
+    for (int a = 0; a < 3; ++a) {
+        out[6 * i + a] = n.lo[a];
+        out[6 * i + 3 + a] = n.hi[a];
+    }
+}
+
+// Rigid per-mesh motion on the device (cfg3): world corner = M * p with
+// M the mesh's 3x4 world_from_object, row r as ((m0*x + m1*y) + m2*z) + m3
+// (no FMA; paper_2309_04581_b200.configs.apply_rigid is the same order),
+// then v0 | e1 = w1 - w0 | e2 = w2 - w0 into the refit staging buffer and the
+// unit normal of face_normals_of (surface.py:169-176 order).
+__global__ void k_rigid_faces(const double* __restrict__ base, const int32_t* __restrict__ mesh_of,
+                              const double* __restrict__ xf, int32_t n_meshes, int32_t n, double* src,
+                              double* normal) {
+    const size_t n3 = 3 * (size_t)n;
+    for (int32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < n; f += gridDim.x * blockDim.x) {
+        const int32_t mi = min(mesh_of[f], n_meshes - 1);
+        const double* m = xf + 12 * (size_t)mi;
+        double w[3][3];
+        for (int c = 0; c < 3; ++c) {
+            const double* p = base + 9 * (size_t)f + 3 * c;
+            for (int r = 0; r < 3; ++r)
+                w[c][r] = ((m[4 * r] * p[0] + m[4 * r + 1] * p[1]) + m[4 * r + 2] * p[2]) + m[4 * r + 3];
+        }
+        double e1[3], e2[3];
+        for (int r = 0; r < 3; ++r) {
+            e1[r] = w[1][r] - w[0][r];
+            e2[r] = w[2][r] - w[0][r];
+            src[3 * (size_t)f + r] = w[0][r];
+            src[n3 + 3 * (size_t)f + r] = e1[r];
+            src[2 * n3 + 3 * (size_t)f + r] = e2[r];
+        }
+        const double nx = e1[1] * e2[2] - e1[2] * e2[1];
+        const double ny = e1[2] * e2[0] - e1[0] * e2[2];
+        const double nz = e1[0] * e2[1] - e1[1] * e2[0];
+        const double len = sqrt((nx * nx + ny * ny) + nz * nz);
+        normal[3 * (size_t)f] = nx / len;
+        normal[3 * (size_t)f + 1] = ny / len;
+        normal[3 * (size_t)f + 2] = nz / len;
+    }
+}
+
+// Blocker staging from the main one (blocker face i = global face map[i]).
+__global__ void k_gather_faces(const double* __restrict__ src, int32_t n, const int32_t* __restrict__ map,
+                               int32_t nb, double* dst) {
+    const size_t n3 = 3 * (size_t)n, b3 = 3 * (size_t)nb;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+        const int32_t f = map[i];
+        for (int k = 0; k < 3; ++k)
+            for (int r = 0; r < 3; ++r) dst[k * b3 + 3 * (size_t)i + r] = src[k * n3 + 3 * (size_t)f + r];
     }
 }
 

@@ -200,4 +200,27 @@ BvhHost build_bvh(int64_t n_faces, const double* v0, const double* e1, const dou
     return out;
 }
 
+BvhHost build_forest(int64_t n_faces, const double* v0, const double* e1, const double* e2,
+                     const std::vector<int32_t>& group_begin) {
+    BvhHost out;
+    out.n_faces = (int32_t)n_faces;
+    for (size_t g = 0; g + 1 < group_begin.size(); ++g) {
+        const int32_t f0 = group_begin[g], nf = group_begin[g + 1] - f0;
+        if (nf <= 0) continue;
+        BvhHost t = build_bvh(nf, v0 + 3 * (size_t)f0, e1 + 3 * (size_t)f0, e2 + 3 * (size_t)f0);
+        const int32_t noff = (int32_t)out.nodes.size(), toff = (int32_t)out.tri_id.size();
+        out.roots.push_back(noff);
+        for (size_t i = 0; i < t.nodes.size(); ++i) {
+            BvhNodeHost nd = t.nodes[i];
+            nd.first += nd.count > 0 ? toff : noff;
+            out.nodes.push_back(nd);
+            out.parent.push_back(t.parent[i] < 0 ? -1 : t.parent[i] + noff);
+        }
+        for (int32_t l : t.leaves) out.leaves.push_back(l + noff);
+        out.tri.insert(out.tri.end(), t.tri.begin(), t.tri.end());
+        for (int32_t id : t.tri_id) out.tri_id.push_back(id + f0);
+    }
+    return out;
+}
+
 }  // namespace hrt

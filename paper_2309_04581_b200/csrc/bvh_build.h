@@ -20,8 +20,16 @@ struct BvhHost {
     std::vector<int32_t> tri_id;    // leaf order -> global face id
     std::vector<int32_t> parent;    // node -> parent (-1 at the root), for GPU refit
     std::vector<int32_t> leaves;    // indices of leaf nodes
+    std::vector<int32_t> roots;     // build_forest: root node of every group's tree
 };
 
 BvhHost build_bvh(int64_t n_faces, const double* v0, const double* e1, const double* e2);
+
+// One tree per group of consecutive faces [group_begin[g], group_begin[g+1]),
+// concatenated (node / triangle indices offset, every root's parent -1). The
+// trees of rigidly moving meshes stay tight under refit; a small top level
+// over their root boxes is rebuilt per frame (hrt.cu).
+BvhHost build_forest(int64_t n_faces, const double* v0, const double* e1, const double* e2,
+                     const std::vector<int32_t>& group_begin);
 
 }  // namespace hrt

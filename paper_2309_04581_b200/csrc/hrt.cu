@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -57,6 +58,11 @@ constexpr bool kTiledFrame = HRT_TILED_FRAME;      // full frames walk 16x16 pix
 struct RefitState {              // device side of a BVH's GPU refit
     int2* wsrc = nullptr;        // float64 node behind each WNode child slot
     int32_t n_w = 0;
+    int32_t w_begin = 0;         // forest: WNodes [0, w_begin) are the top level over the roots
+    std::vector<int32_t> roots;  // forest: root node of every group's tree
+    std::vector<int32_t> root_ref;   // and its WNode reference
+    int32_t* d_roots = nullptr;
+    double* d_rootbox = nullptr; // gathered root boxes (6 doubles each)
     int32_t* parent = nullptr;
     int32_t* leaves = nullptr;
     int32_t* visits = nullptr;
@@ -99,6 +105,9 @@ struct hrt_handle {
     uint32_t* occ_dev = nullptr;
     int64_t occ_words = 0;
     unsigned long long tex = 0;
+    double* rigid_base = nullptr;   // hrt_set_rigid_base: object-space corners, global face order
+    std::vector<int32_t> mesh_of_host;
+    int32_t* blk_map = nullptr;     // blocker face -> global face
     int64_t tab_entries = 0;
     int shadow_blocks = 0;
     // hrt_set_profile: event pair per launch, folded into stage_ms
@@ -157,12 +166,21 @@ int setup_refit(hrt_handle* h, const hrt::BvhHost& b, RefitState& r) {
 
 // K11: upload the new world-space faces, permute them into leaf order and
 // refit the boxes bottom-up on the device.
+int refit_from_src(hrt_handle* h, const hrt::BvhHost& b, RefitState& r, DevBvh& dev);
+void build_tlas(const std::vector<hrt::BvhNodeHost>& box, const std::vector<int32_t>& ref, WNode* w);
+
 int refit_gpu(hrt_handle* h, const hrt::BvhHost& b, RefitState& r, DevBvh& dev, const double* v0,
               const double* e1, const double* e2) {
     const size_t n3 = 3 * (size_t)b.n_faces;
     CK(cudaMemcpy(r.src, v0, n3 * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(r.src + n3, e1, n3 * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(r.src + 2 * n3, e2, n3 * 8, cudaMemcpyHostToDevice));
+    return refit_from_src(h, b, r, dev);
+}
+
+// Refit from faces already in r.src (v0 | e1 | e2, global face order).
+int refit_from_src(hrt_handle* h, const hrt::BvhHost& b, RefitState& r, DevBvh& dev) {
+    const size_t n3 = 3 * (size_t)b.n_faces;
     CK(cudaMemset(r.visits, 0, b.nodes.size() * 4));
     const unsigned g1 = (unsigned)std::min<int64_t>((b.n_faces + 255) / 256, 148 * 16);
     bvh::k_permute_tris<<<g1, 256>>>(r.src, r.src + n3, r.src + 2 * n3, dev.tri_id, b.n_faces,
@@ -173,8 +191,25 @@ int refit_gpu(hrt_handle* h, const hrt::BvhHost& b, RefitState& r, DevBvh& dev, 
                               r.visits);
     CK(cudaGetLastError());
     const unsigned g3 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((r.n_w + 255) / 256, 148 * 16));
-    bvh::k_wsync<<<g3, 256>>>(const_cast<WNode*>(dev.wnodes), r.wsrc, dev.nodes, r.n_w);
+    bvh::k_wsync<<<g3, 256>>>(const_cast<WNode*>(dev.wnodes), r.wsrc, dev.nodes, r.w_begin, r.n_w);
     CK(cudaGetLastError());
+    if (!r.roots.empty()) {          // forest: new root boxes -> rebuild the top level
+        const int32_t G = (int32_t)r.roots.size();
+        bvh::k_root_boxes<<<(G + 255) / 256, 256>>>(dev.nodes, r.d_roots, G, r.d_rootbox);
+        CK(cudaGetLastError());
+        std::vector<double> rb(6 * (size_t)G);
+        CK(cudaMemcpy(rb.data(), r.d_rootbox, rb.size() * 8, cudaMemcpyDeviceToHost));
+        std::vector<hrt::BvhNodeHost> boxes(G);
+        for (int32_t g = 0; g < G; ++g)
+            for (int a = 0; a < 3; ++a) {
+                boxes[g].lo[a] = rb[6 * g + a];
+                boxes[g].hi[a] = rb[6 * g + 3 + a];
+            }
+        std::vector<WNode> top(G - 1);
+        build_tlas(boxes, r.root_ref, top.data());
+        CK(cudaMemcpy(const_cast<WNode*>(dev.wnodes), top.data(), top.size() * sizeof(WNode),
+                      cudaMemcpyHostToDevice));
+    }
     return HRT_OK;
 }
 
@@ -202,32 +237,76 @@ void wbox(const hrt::BvhNodeHost& n, float lo[3], float hi[3]) {
     }
 }
 
+void wset(WNode& x, const hrt::BvhNodeHost* n0, const hrt::BvhNodeHost* n1, int32_t r0, int32_t r1) {
+    float l0[3], h0[3], l1[3], h1[3];
+    for (int a = 0; a < 3; ++a) l0[a] = h0[a] = l1[a] = h1[a] = 1e30f;
+    if (n0) wbox(*n0, l0, h0);
+    if (n1) wbox(*n1, l1, h1);
+    x.a = make_float4(l0[0], l0[1], l0[2], h0[0]);
+    x.b = make_float4(h0[1], h0[2], l1[0], l1[1]);
+    x.c = make_float4(l1[2], h1[0], h1[1], h1[2]);
+    x.r = make_int4(r0, r1, 0, 0);
+}
+
+// Top level of a forest over its G root boxes: G-1 WNodes written to w[0..),
+// root at 0, median splits on the widest centroid axis (rebuilt per frame).
+void build_tlas(const std::vector<hrt::BvhNodeHost>& box, const std::vector<int32_t>& ref, WNode* w) {
+    std::vector<int32_t> it(box.size());
+    for (size_t i = 0; i < it.size(); ++i) it[i] = (int32_t)i;
+    int32_t next = 0;
+    std::function<std::pair<int32_t, hrt::BvhNodeHost>(int32_t, int32_t)> rec =
+        [&](int32_t b, int32_t e) -> std::pair<int32_t, hrt::BvhNodeHost> {
+        if (e - b == 1) return {ref[it[b]], box[it[b]]};
+        const int32_t t = next++;
+        double clo[3] = {INFINITY, INFINITY, INFINITY}, chi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int32_t i = b; i < e; ++i)
+            for (int a = 0; a < 3; ++a) {
+                const double c = 0.5 * (box[it[i]].lo[a] + box[it[i]].hi[a]);
+                clo[a] = std::min(clo[a], c);
+                chi[a] = std::max(chi[a], c);
+            }
+        int ax = 0;
+        for (int a = 1; a < 3; ++a)
+            if (chi[a] - clo[a] > chi[ax] - clo[ax]) ax = a;
+        const int32_t m = b + (e - b) / 2;
+        std::nth_element(it.begin() + b, it.begin() + m, it.begin() + e, [&](int32_t x, int32_t y) {
+            return box[x].lo[ax] + box[x].hi[ax] < box[y].lo[ax] + box[y].hi[ax];
+        });
+        auto L = rec(b, m), R = rec(m, e);
+        wset(w[t], &L.second, &R.second, L.first, R.first);
+        hrt::BvhNodeHost u;
+        for (int a = 0; a < 3; ++a) {
+            u.lo[a] = std::min(L.second.lo[a], R.second.lo[a]);
+            u.hi[a] = std::max(L.second.hi[a], R.second.hi[a]);
+        }
+        return {t, u};
+    };
+    rec(0, (int32_t)box.size());
+}
+
 // float32-culling tree over the same leaves: one WNode per inner float64
 // node (a root leaf gets a WNode with an empty second child); src records
-// the float64 node behind each child slot for k_wsync after refits.
-void build_wnodes(const hrt::BvhHost& b, std::vector<WNode>& w, std::vector<int2>& src) {
+// the float64 node behind each child slot for k_wsync after refits. A
+// forest (b.roots, >= 2 trees) gets a top level over the roots in
+// WNodes [0, G-1) (r.w_begin), its trees' WNodes after it.
+void build_wnodes(const hrt::BvhHost& b, std::vector<WNode>& w, std::vector<int2>& src, RefitState& r) {
     const auto& nd = b.nodes;
+    const bool forest = b.roots.size() >= 2;
+    const int32_t T = forest ? (int32_t)b.roots.size() - 1 : 0;
     std::vector<int32_t> widx(nd.size(), -1);
-    int32_t nw = 0;
+    int32_t nw = T;
     for (size_t i = 0; i < nd.size(); ++i)
         if (nd[i].count == 0) widx[i] = nw++;
     auto ref = [&](int32_t c) -> int32_t {
         return nd[c].count > 0 ? ~((nd[c].first << 3) | nd[c].count) : widx[c];
     };
-    auto fill = [&](WNode& x, int32_t c0, int32_t c1) {
-        float l0[3], h0[3], l1[3], h1[3];
-        for (int a = 0; a < 3; ++a) l0[a] = h0[a] = l1[a] = h1[a] = 1e30f;
-        if (c0 >= 0) wbox(nd[c0], l0, h0);
-        if (c1 >= 0) wbox(nd[c1], l1, h1);
-        x.a = make_float4(l0[0], l0[1], l0[2], h0[0]);
-        x.b = make_float4(h0[1], h0[2], l1[0], l1[1]);
-        x.c = make_float4(l1[2], h1[0], h1[1], h1[2]);
-        x.r = make_int4(c0 >= 0 ? ref(c0) : -1, c1 >= 0 ? ref(c1) : -1, 0, 0);
-    };
-    if (nd[0].count > 0) {           // whole mesh in one leaf
+    r.w_begin = T;
+    r.roots.clear();
+    r.root_ref.clear();
+    if (!forest && nd[0].count > 0) {           // whole mesh in one leaf
         w.assign(1, WNode{});
         src.assign(1, make_int2(0, -1));
-        fill(w[0], 0, -1);
+        wset(w[0], &nd[0], nullptr, ref(0), -1);
         return;
     }
     w.assign(nw, WNode{});
@@ -235,27 +314,40 @@ void build_wnodes(const hrt::BvhHost& b, std::vector<WNode>& w, std::vector<int2
     for (size_t i = 0; i < nd.size(); ++i) {
         if (nd[i].count != 0) continue;
         const int32_t c = nd[i].first;
-        fill(w[widx[i]], c, c + 1);
+        wset(w[widx[i]], &nd[c], &nd[c + 1], ref(c), ref(c + 1));
         src[widx[i]] = make_int2(c, c + 1);
+    }
+    if (forest) {
+        std::vector<hrt::BvhNodeHost> boxes;
+        for (int32_t rt : b.roots) {
+            r.roots.push_back(rt);
+            r.root_ref.push_back(ref(rt));
+            boxes.push_back(nd[rt]);
+        }
+        build_tlas(boxes, r.root_ref, w.data());
     }
 }
 
-int upload_bvh(hrt_handle* h, const hrt::BvhHost& b, DevBvh& out, int2** wsrc, int32_t* n_w) {
+int upload_bvh(hrt_handle* h, const hrt::BvhHost& b, DevBvh& out, RefitState& r) {
     out.n_faces = b.n_faces;
     out.nodes = nullptr; out.tri = nullptr; out.tri_id = nullptr; out.wnodes = nullptr;
-    *wsrc = nullptr;
-    *n_w = 0;
+    r.wsrc = nullptr;
+    r.n_w = 0;
     if (b.n_faces == 0) return HRT_OK;
     {
         std::vector<WNode> w;
         std::vector<int2> src;
-        build_wnodes(b, w, src);
+        build_wnodes(b, w, src, r);
         WNode* dw;
         int rc;
         if ((rc = h->upload(w.data(), w.size(), &dw))) return rc;
-        if ((rc = h->upload(src.data(), src.size(), wsrc))) return rc;
+        if ((rc = h->upload(src.data(), src.size(), &r.wsrc))) return rc;
         out.wnodes = dw;
-        *n_w = (int32_t)w.size();
+        r.n_w = (int32_t)w.size();
+        if (!r.roots.empty()) {
+            if ((rc = h->upload(r.roots.data(), r.roots.size(), &r.d_roots))) return rc;
+            if ((rc = h->alloc(r.roots.size() * 6 * 8, reinterpret_cast<void**>(&r.d_rootbox)))) return rc;
+        }
     }
     static_assert(sizeof(BvhNode) == sizeof(hrt::BvhNodeHost), "node layout");
     BvhNode* nodes;
@@ -817,8 +909,9 @@ int hrt_create(const hrt_scene_desc* d, hrt_handle** out) {
     int rc;
     h->bvh = hrt::build_bvh(d->n_faces, d->v0, d->e1, d->e2);
     h->blk = hrt::build_bvh(d->n_blockers, d->bv0, d->be1, d->be2);
-    if ((rc = upload_bvh(h, h->bvh, sc.bvh, &h->rf.wsrc, &h->rf.n_w))) return bail(rc);
-    if ((rc = upload_bvh(h, h->blk, sc.blockers, &h->rfb.wsrc, &h->rfb.n_w))) return bail(rc);
+    if ((rc = upload_bvh(h, h->bvh, sc.bvh, h->rf))) return bail(rc);
+    if ((rc = upload_bvh(h, h->blk, sc.blockers, h->rfb))) return bail(rc);
+    h->mesh_of_host.assign(d->mesh_of, d->mesh_of + d->n_faces);
     if ((rc = setup_refit(h, h->bvh, h->rf))) return bail(rc);
     if ((rc = setup_refit(h, h->blk, h->rfb))) return bail(rc);
     double *normal, *emission;
@@ -1121,6 +1214,76 @@ int hrt_refit(hrt_handle* h, const double* v0, const double* e1, const double* e
     }
     CK(cudaDeviceSynchronize());
     return HRT_OK;
+}
+
+// Rebuild a tree as a forest of per-mesh trees (group = mesh of each face in
+// this tree's face order), re-upload it and its refit state.
+int to_forest(hrt_handle* h, hrt::BvhHost& b, RefitState& r, DevBvh& dev, const std::vector<int32_t>& group) {
+    const int32_t n = b.n_faces;
+    if (n == 0) return HRT_OK;
+    std::vector<double> v0(3 * (size_t)n), e1(3 * (size_t)n), e2(3 * (size_t)n);
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t f = b.tri_id[i];
+        std::memcpy(&v0[3 * (size_t)f], &b.tri[9 * (size_t)i], 24);
+        std::memcpy(&e1[3 * (size_t)f], &b.tri[9 * (size_t)i + 3], 24);
+        std::memcpy(&e2[3 * (size_t)f], &b.tri[9 * (size_t)i + 6], 24);
+    }
+    std::vector<int32_t> begin;
+    for (int32_t f = 0; f < n; ++f)
+        if (f == 0 || group[f] != group[f - 1]) begin.push_back(f);
+    begin.push_back(n);
+    if (begin.size() < 3) return HRT_OK;              // one mesh: the tree already refits tightly
+    b = hrt::build_forest(n, v0.data(), e1.data(), e2.data(), begin);
+    int rc;
+    if ((rc = upload_bvh(h, b, dev, r))) return rc;
+    return setup_refit(h, b, r);
+}
+
+int hrt_set_rigid_base(hrt_handle* h, const double* corners, const int32_t* blocker_faces) {
+    if (!h || (h->bvh.n_faces && !corners)) return fail(HRT_EINVAL, "null argument");
+    if (h->blk.n_faces && !blocker_faces) return fail(HRT_EINVAL, "blocker face map required");
+    int rc;
+    if (h->rf.roots.empty() && h->rfb.roots.empty()) {
+        // rigid meshes: one tree per mesh + a per-frame top level, so refits stay tight
+        if ((rc = to_forest(h, h->bvh, h->rf, h->sc.bvh, h->mesh_of_host))) return rc;
+        std::vector<int32_t> bg(h->blk.n_faces);
+        for (int32_t i = 0; i < h->blk.n_faces; ++i) bg[i] = h->mesh_of_host[blocker_faces[i]];
+        if ((rc = to_forest(h, h->blk, h->rfb, h->sc.blockers, bg))) return rc;
+    }
+    if (!h->rigid_base) {
+        if ((rc = h->alloc((size_t)std::max(1, h->bvh.n_faces) * 9 * 8, reinterpret_cast<void**>(&h->rigid_base))))
+            return rc;
+        if ((rc = h->alloc((size_t)std::max(1, h->blk.n_faces) * 4, reinterpret_cast<void**>(&h->blk_map))))
+            return rc;
+    }
+    CK(cudaMemcpy(h->rigid_base, corners, (size_t)h->bvh.n_faces * 9 * 8, cudaMemcpyHostToDevice));
+    if (h->blk.n_faces)
+        CK(cudaMemcpy(h->blk_map, blocker_faces, (size_t)h->blk.n_faces * 4, cudaMemcpyHostToDevice));
+    return HRT_OK;
+}
+
+int hrt_refit_rigid(hrt_handle* h, const double* xf, int32_t n_meshes) {
+    if (!h || !xf) return fail(HRT_EINVAL, "null argument");
+    if (!h->rigid_base) return fail(HRT_EINVAL, "hrt_set_rigid_base first");
+    if (h->bvh.n_faces == 0) return HRT_OK;
+    double* dxf = nullptr;
+    CK(cudaMalloc(&dxf, (size_t)n_meshes * 12 * 8));
+    CK(cudaMemcpy(dxf, xf, (size_t)n_meshes * 12 * 8, cudaMemcpyHostToDevice));
+    const int32_t n = h->bvh.n_faces;
+    const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    bvh::k_rigid_faces<<<g, 256>>>(h->rigid_base, h->sc.mesh_of, dxf, n_meshes, n, h->rf.src, h->d_normal);
+    CK(cudaGetLastError());
+    int rc = refit_from_src(h, h->bvh, h->rf, h->sc.bvh);
+    if (rc == HRT_OK && h->blk.n_faces) {
+        const int32_t nb = h->blk.n_faces;
+        const unsigned gb = (unsigned)std::min<int64_t>((nb + 255) / 256, 148 * 16);
+        bvh::k_gather_faces<<<gb, 256>>>(h->rf.src, n, h->blk_map, nb, h->rfb.src);
+        CK(cudaGetLastError());
+        rc = refit_from_src(h, h->blk, h->rfb, h->sc.blockers);
+    }
+    CK(cudaDeviceSynchronize());
+    cudaFree(dxf);
+    return rc;
 }
 
 int hrt_field_sample(hrt_handle* h, const double* points, const double* dirs, int64_t n, float* sigma,

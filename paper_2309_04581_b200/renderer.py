@@ -117,6 +117,34 @@ class Renderer:
         _lib.check(self.lib.hrt_refit(self.handle, *ptrs), "hrt_refit")
         self.pack = pk
 
+    def set_rigid_base(self, object_vertices, indices, emissive=None):
+        """Object-space geometry for refit_rigid: per mesh (in scene order) its
+        object vertices and faces; `emissive` flags exclude meshes from the
+        blocker tree as pack_scene does."""
+        corners = np.concatenate([np.asarray(v, np.float64)[np.asarray(f).reshape(-1, 3)].reshape(-1, 9)
+                                  for v, f in zip(object_vertices, indices)])
+        emissive = emissive or [False] * len(indices)
+        blk, base = [], 0
+        for f, e in zip(indices, emissive):
+            nf = len(np.asarray(f).reshape(-1, 3))
+            if not e:
+                blk.append(np.arange(base, base + nf, dtype=np.int32))
+            base += nf
+        blk = np.concatenate(blk) if blk else np.zeros(0, np.int32)
+        if len(corners) != len(self.pack["v0"]) or len(blk) != len(self.pack["bv0"]):
+            raise ValueError("rigid base does not match the scene's faces")
+        corners = np.ascontiguousarray(corners)
+        self._rigid_keep = (corners, blk)
+        _lib.check(self.lib.hrt_set_rigid_base(self.handle, corners.ctypes.data_as(ctypes.c_void_p),
+                                               blk.ctypes.data_as(ctypes.c_void_p)), "hrt_set_rigid_base")
+
+    def refit_rigid(self, transforms):
+        """Move every mesh by its 3x4 world_from_object (n_meshes, 3, 4) and
+        refit both trees on the GPU (hrt_refit_rigid)."""
+        xf = np.ascontiguousarray(transforms, np.float64).reshape(-1, 12)
+        _lib.check(self.lib.hrt_refit_rigid(self.handle, xf.ctypes.data_as(ctypes.c_void_p), len(xf)),
+                   "hrt_refit_rigid")
+
     # ------------------------------------------------------------ probes
     def field_sample(self, points, dirs=None, use_occupancy=False):
         n = points.shape[0]
