@@ -20,7 +20,10 @@ namespace hrt {
 namespace {
 
 constexpr int kBins = 16;
-constexpr int kLeaf = 4;
+#ifndef HRT_BVH_LEAF
+#define HRT_BVH_LEAF 1
+#endif
+constexpr int kLeaf = HRT_BVH_LEAF;   // max triangles per leaf (<= 7: 3-bit count in WNode refs)
 constexpr int kSahDepth = 32;   // median splits below this: depth <= 32 + log2(n/4) < kStack
 
 struct Box {
