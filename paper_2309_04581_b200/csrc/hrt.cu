@@ -35,7 +35,10 @@ int fail(int code, const std::string& msg) {
             return fail(HRT_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
     } while (0)
 
-constexpr int64_t kMaxPaths = int64_t(1) << 20;   // paths per wavefront chunk
+#ifndef HRT_MAX_PATHS_LOG2
+#define HRT_MAX_PATHS_LOG2 22
+#endif
+constexpr int64_t kMaxPaths = int64_t(1) << HRT_MAX_PATHS_LOG2;   // paths per wavefront chunk
 constexpr int kThreads = 256;
 constexpr int kTimedLaunches = 1024;
 constexpr int kIoChunks = 4;                       // pieces of the e2e frame read-back
@@ -43,7 +46,10 @@ constexpr int kIoChunks = 4;                       // pieces of the e2e frame re
 #define HRT_SHADOW_QUEUE 1
 #endif
 constexpr bool kShadowQueue = HRT_SHADOW_QUEUE;   // shadow rays: set-up pass + persistent tracer
-constexpr int64_t kBatchCap = int64_t(1) << 24;   // samples per march round
+#ifndef HRT_BATCH_CAP_LOG2
+#define HRT_BATCH_CAP_LOG2 26
+#endif
+constexpr int64_t kBatchCap = int64_t(1) << HRT_BATCH_CAP_LOG2;   // samples per march round
 #ifndef HRT_TEX_LEVELS
 #define HRT_TEX_LEVELS 8
 #endif
