@@ -1001,12 +1001,17 @@ int hrt_set_profile(hrt_handle* h, int32_t on) {
 
 int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed, int32_t mode,
                const int32_t* pixels, int64_t n_pixels, double* out, hrt_stats* stats, void* stream) {
-    if (!h || !cam || !out) return fail(HRT_EINVAL, "null argument");
+    if (!h || !cam) return fail(HRT_EINVAL, "null argument");
     if (spp < 1) return fail(HRT_EINVAL, "spp must be >= 1");
     if (mode < 0 || mode > 2) return fail(HRT_EINVAL, "bad mode");
     if (cam->width < 1 || cam->height < 1) return fail(HRT_EINVAL, "bad resolution");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t total_pix = pixels ? n_pixels : (int64_t)cam->width * cam->height;
+    if (pixels && total_pix <= 0) {            // empty pixel list (e.g. a rank without tiles)
+        if (stats) *stats = hrt_stats{};
+        return HRT_OK;
+    }
+    if (!out) return fail(HRT_EINVAL, "null argument");
     const int64_t chunk_pix = std::max<int64_t>(1, kMaxPaths / spp);
     int rc;
     if ((rc = ensure_state(h, std::min<int64_t>(total_pix, chunk_pix) * spp))) return rc;

@@ -74,6 +74,9 @@ class Renderer:
         n = cam.width * cam.height if pixels is None else int(pixels.numel())
         if out is None:
             out = torch.empty((n, 3), dtype=torch.float64, device=self.device)
+        if n == 0:                                   # a rank without tiles
+            self.last_stats = _lib.Stats().as_dict()
+            return out
         stats = _lib.Stats()
         rc = self.lib.hrt_render(self.handle, ctypes.byref(cam), int(spp), int(seed) & (2**64 - 1),
                                  int(mode), _dptr(pixels), n, _dptr(out), ctypes.byref(stats),

@@ -298,3 +298,34 @@ def test_dense_grid_scenes_match_oracle(cuda, name):
     assert np.abs(out - want).max() < 1e-9
     assert out.mean() > 0.01
     r.close()
+
+
+# ------------------------------------------------------- frame edge cases
+
+@pytest.mark.parametrize("res,spp", [((37, 21), 1), ((37, 21), 4), ((1, 1), 3), ((17, 33), 2)])
+def test_full_frame_odd_shapes_and_spp(cuda, res, spp):
+    """Full frames whose sides are not multiples of the 16x16 slot tiles
+    (partial edge tiles of tiled_pixel), stratified (4) and plain (2, 3) spp."""
+    field = NeuralField.random(3, n_levels=8, n_features=2, log2_table=12, n_min=16, n_max=128,
+                               occupancy_res=32)
+    v, f = assets.icosphere(0.4, 2)
+    cam = Camera(Transform.look_at((0.4, 0.3, 3), (0, 0, 0)), math.radians(40.0), res)
+    scene = make_scene(field=field, meshes=[TriangleMesh(v, f, Dielectric(1.5))], camera=cam,
+                       spp=spp, n_bounces=3, march_step=configs.MARCH_STEP, seed=4)
+    r = Renderer(scene)
+    out = r.render_pixels(cam, spp, 4).cpu().numpy()
+    st = {}
+    want = tracer.render(r.pack, pack_camera(cam), spp, 4, stats=st).reshape(-1, 3)
+    assert out.shape == want.shape
+    assert np.abs(out - want).max() < 1e-3
+    assert r.last_stats["nerf_samples"] == st["nerf_samples"]
+    r.close()
+
+
+def test_empty_pixel_list(cuda):
+    scene = configs.cfg0()
+    r = Renderer(scene)
+    out = r.render_pixels(scene.camera, 1, 0, pixels=torch.zeros(0, dtype=torch.int32, device=cuda))
+    assert out.shape == (0, 3)
+    assert r.last_stats["paths"] == 0
+    r.close()
