@@ -159,7 +159,9 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
                const int32_t* pixels, int64_t n_pixels, double* out, hrt_stats* stats,
                void* stream);
 
-/* Same with host pixels / host out; copies inside, synchronous. */
+/* Same with host pixels / host out; copies inside, synchronous. Page-locked
+ * (cudaMallocHost / cudaHostRegister) buffers are DMA'd directly, pageable
+ * ones are staged through pinned buffers owned by the handle. */
 int hrt_render_host(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
                     int32_t mode, const int32_t* pixels, int64_t n_pixels, double* out,
                     hrt_stats* stats);

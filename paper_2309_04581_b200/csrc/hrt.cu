@@ -648,6 +648,9 @@ int ensure_io(hrt_handle* h, int64_t npx) {
     return HRT_OK;
 }
 
+// Is a caller buffer page-locked (then it is DMA'd directly, else staged)?
+bool host_pinned(const void* p);
+
 // memcpy split over a few host threads (one core copies ~10 GB/s; the frame
 // read-back of the e2e path is 15 MB at 800x800).
 void par_copy(char* dst, const char* src, size_t len) {
@@ -663,6 +666,15 @@ void par_copy(char* dst, const char* src, size_t len) {
     }
     std::memcpy(dst, src, std::min(part, len));
     for (auto& t : ts) t.join();
+}
+
+bool host_pinned(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;               // cudaMallocHost / cudaHostRegister memory
 }
 
 int read_counter(hrt_handle* h, int idx, cudaStream_t st, int32_t* v) {
@@ -1185,26 +1197,39 @@ int hrt_render_host(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t 
     int rc;
     if ((rc = ensure_io(h, npx))) return rc;
     cudaStream_t st = h->io_stream;
-    if (pixels) {       // stage through pinned memory so the H2D is a true async DMA
-        par_copy(reinterpret_cast<char*>(h->io_pix_host), reinterpret_cast<const char*>(pixels), (size_t)npx * 4);
-        CK(cudaMemcpyAsync(h->io_pix, h->io_pix_host, (size_t)npx * 4, cudaMemcpyHostToDevice, st));
+    const size_t in_bytes = (size_t)npx * 4, out_bytes = (size_t)npx * 24;
+    // page-locked caller buffers are DMA'd directly; pageable ones are staged
+    // through the handle's pinned buffers
+    const bool in_direct = pixels && host_pinned(pixels);
+    const bool out_direct = host_pinned(out);
+    if (pixels) {
+        if (in_direct) {
+            CK(cudaMemcpyAsync(h->io_pix, pixels, in_bytes, cudaMemcpyHostToDevice, st));
+        } else {
+            par_copy(reinterpret_cast<char*>(h->io_pix_host), reinterpret_cast<const char*>(pixels), in_bytes);
+            CK(cudaMemcpyAsync(h->io_pix, h->io_pix_host, in_bytes, cudaMemcpyHostToDevice, st));
+        }
     }
     rc = hrt_render(h, cam, spp, seed, mode, pixels ? h->io_pix : nullptr, npx, h->io_out, stats, st);
     if (rc == HRT_OK || rc == HRT_ENONFINITE) {
-        // frame back in kIoChunks DMA pieces; the pinned -> caller copy of piece k
-        // (split over host threads) overlaps the DMA of pieces k+1..
-        const size_t bytes = (size_t)npx * 24;
-        const size_t piece = (bytes / kIoChunks + 4095) & ~size_t(4095);
+        if (out_direct) {
+            CK(cudaMemcpyAsync(out, h->io_out, out_bytes, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            return rc;
+        }
+        // staging: the frame comes back in kIoChunks DMA pieces; the pinned ->
+        // caller copy of piece k overlaps the DMA of pieces k+1..
+        const size_t piece = (out_bytes / kIoChunks + 4095) & ~size_t(4095);
         int nk = 0;
-        for (size_t off = 0; off < bytes; off += piece, ++nk) {
-            const size_t len = std::min(piece, bytes - off);
+        for (size_t off = 0; off < out_bytes; off += piece, ++nk) {
+            const size_t len = std::min(piece, out_bytes - off);
             CK(cudaMemcpyAsync(reinterpret_cast<char*>(h->io_out_host) + off,
                                reinterpret_cast<const char*>(h->io_out) + off, len, cudaMemcpyDeviceToHost, st));
             CK(cudaEventRecord(h->io_ev[nk], st));
         }
         for (int k = 0; k < nk; ++k) {
             CK(cudaEventSynchronize(h->io_ev[k]));
-            const size_t off = (size_t)k * piece, len = std::min(piece, bytes - off);
+            const size_t off = (size_t)k * piece, len = std::min(piece, out_bytes - off);
             par_copy(reinterpret_cast<char*>(out) + off, reinterpret_cast<const char*>(h->io_out_host) + off, len);
         }
     }

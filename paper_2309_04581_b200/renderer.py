@@ -85,8 +85,16 @@ class Renderer:
         _lib.check(rc, "hrt_render")
         return out
 
+    @staticmethod
+    def pinned(shape, dtype):
+        """A numpy array in page-locked host memory (render_host DMAs it
+        directly; the array keeps its pinned storage alive)."""
+        tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.int32): torch.int32}[np.dtype(dtype)]
+        return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+
     def render_host(self, camera, spp, seed, mode=_lib.MODE_HYBRID, pixels=None, out=None):
-        """Same through host buffers (numpy in/out, copies inside the call)."""
+        """Same through host buffers (numpy in/out, copies inside the call;
+        page-locked buffers, see `pinned`, are DMA'd without staging)."""
         cam = _lib.camera_desc(camera if isinstance(camera, dict) else pack_camera(camera))
         pix = None if pixels is None else np.ascontiguousarray(pixels, np.int32)
         n = cam.width * cam.height if pix is None else len(pix)

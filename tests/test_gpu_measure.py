@@ -58,3 +58,20 @@ def test_stats_do_not_overflow_int32():
     assert s["nerf_samples"] > 2 ** 31
     assert s["shadow_rays"] > 2 ** 31
     r.close()
+
+
+def test_render_host_pinned_and_pageable_agree():
+    """hrt_render_host: pinned caller buffers (direct DMA) and pageable ones
+    (staged) give the device path's frame bit for bit."""
+    scene = configs.cfg0()
+    r = Renderer(scene)
+    dev = r.render_pixels(scene.camera, 1, 0).cpu().numpy()
+    pageable = r.render_host(scene.camera, 1, 0)
+    out = Renderer.pinned((64 * 64, 3), np.float64)
+    r.render_host(scene.camera, 1, 0, out=out)
+    assert np.array_equal(dev, pageable) and np.array_equal(dev, out)
+    pix = Renderer.pinned((100,), np.int32)
+    pix[:] = np.arange(100, 200)
+    sub = r.render_host(scene.camera, 1, 0, pixels=pix)
+    assert np.array_equal(sub, dev[100:200])
+    r.close()
