@@ -6,7 +6,9 @@ an L16/T2^19 hash-grid NeRF, 800x800, 1 spp, 4 bounces, 100 cameras).
 One step = one full 800x800 frame from camera (step mod 100), rendered by
 the sm_100a kernels through the C ABI with scene and network resident in
 HBM. With N GPUs (torchrun, one rank per GPU) the frame is split into 16x16
-pixel tiles dealt round-robin to ranks and gathered to rank 0 over NCCL
+pixel tiles dealt round-robin to ranks; every rank's accumulate kernel stores
+its pixels straight into rank 0's frame over peer memory (CUDA IPC, NVLink)
+- `--gather nccl` uses an NCCL all-gather instead
 (strong scaling: the frame is fixed). `--impl reference` times the CPU
 oracle port of the reference path (oracle/, numpy) on the host cores instead.
 
@@ -42,6 +44,8 @@ def parse():
     ap.add_argument("--cpu-tiles", type=int, default=0,
                     help="16x16 tiles per CPU-baseline sample (0 = 2 per worker process)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gather", choices=["peer", "nccl"], default="peer",
+                    help="frame assembly: peer-memory stores from the render (default) or NCCL all-gather")
     return ap.parse_args()
 
 
@@ -267,12 +271,19 @@ def run_ours(args, rank, world, local):
 
     from paper_2309_04581_b200 import configs
     from paper_2309_04581_b200.renderer import Renderer
-    from paper_2309_04581_b200.tiles import FrameGather, tile_pixels
+    from paper_2309_04581_b200.tiles import FrameGather, PeerFrame, tile_pixels
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; HRT_DIST_BACKEND=gloo lets several ranks share one GPU to test the
+    # multi-rank flow where only one device exists (timings then mean nothing)
+    dev_index = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    backend = os.environ.get("HRT_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     scene = configs.cfg1()
     cams = configs.cfg1_cameras()
     field = scene.field
@@ -283,6 +294,7 @@ def run_ours(args, rank, world, local):
     n_local = len(pix_host)
     gather = FrameGather(w, h, rank, world, dev)
     out = gather.local
+    peer = PeerFrame(w, h, rank, world) if args.gather == "peer" else None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
@@ -292,9 +304,14 @@ def run_ours(args, rank, world, local):
             flush.fill_(float(k))          # evict L2 between timed steps (outside the events)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-        r.render_pixels(cam, 1, 0, pixels=pix, out=out[:n_local])
-        st = dict(r.last_stats)
-        gather.gather()                    # frame assembled on rank 0 (NCCL all-gather)
+        if peer is not None:               # pixels stored into rank 0's frame (peer memory)
+            r.render_pixels(cam, 1, 0, pixels=pix, frame_ptr=peer.ptr)
+            st = dict(r.last_stats)
+            peer.done()
+        else:
+            r.render_pixels(cam, 1, 0, pixels=pix, out=out[:n_local])
+            st = dict(r.last_stats)
+            gather.gather()                # frame assembled on rank 0 (NCCL all-gather)
         if timed:
             e1.record(stream)
             e1.synchronize()
@@ -306,7 +323,7 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev_index)
     clocks.start()
     t_wall = time.perf_counter()
     steps = [step(args.warmup + k, True) for k in range(args.steps)]
@@ -381,7 +398,10 @@ def run_ours(args, rank, world, local):
             "mrays_per_s": tot_paths / (max_ms * 1e-3) / 1e6,
             "nerf_samples_per_frame": tot_samples / args.steps,
             "config": {"workload": WORKLOAD, "frame": [w, h], "tile": TILE,
-                       "parallelism": f"pixel tiles round-robin over {world} GPU(s), NCCL all-gather to rank 0",
+                       "parallelism": f"16x16 pixel tiles round-robin over {world} GPU(s); " + (
+                           "each rank's k_accumulate stores its pixels into rank 0's frame over peer memory "
+                           "(CUDA IPC / NVLink), then a barrier" if peer is not None
+                           else "NCCL all-gather to rank 0"),
                        "l2": "256 MB buffer written before every timed step, outside the CUDA-event window",
                        "wall_s_timed_region": t_wall},
             "gpu_launches": int(launches),
@@ -418,6 +438,8 @@ def run_ours(args, rank, world, local):
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_block(args.cpu_tiles)
         print(json.dumps(line), flush=True)
+    if peer is not None:
+        peer.close()
     r.close()
     if world > 1:
         dist.destroy_process_group()

@@ -159,6 +159,12 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
                const int32_t* pixels, int64_t n_pixels, double* out, hrt_stats* stats,
                void* stream);
 
+/* mode flag: `out` is a raster (w*h, 3) frame indexed by global pixel id
+ * instead of (n_pixels, 3) in list order - e.g. rank 0's frame mapped into
+ * this process with hrt_ipc_open, so the multi-GPU frame assembly is the
+ * accumulate kernel's own stores over NVLink (no gather collective). */
+#define HRT_OUT_BY_PIXEL 0x100
+
 /* Same with host pixels / host out; copies inside, synchronous. Page-locked
  * (cudaMallocHost / cudaHostRegister) buffers are DMA'd directly, pageable
  * ones are staged through pinned buffers owned by the handle. */
@@ -216,6 +222,15 @@ int hrt_set_profile(hrt_handle* h, int32_t on);
  * input); PFM stores it as is, like encode_pfm. */
 int hrt_finalize(int32_t width, int32_t height, const double* src, const int32_t* pixel, int64_t n,
                  int32_t hdr, uint8_t* out, int64_t cap, int64_t* nbytes, void* stream);
+
+/* Peer frame plumbing (tiles.PeerFrame): a cudaMalloc'd buffer, its CUDA
+ * IPC handle (64 bytes) and the mapping of a peer's buffer into this process
+ * (peer access enabled lazily; NVLink / NVSwitch between GPUs). */
+int hrt_buffer_alloc(int64_t bytes, void** ptr);
+int hrt_buffer_free(void* ptr);
+int hrt_ipc_handle(const void* ptr, uint8_t* handle64);
+int hrt_ipc_open(const uint8_t* handle64, void** ptr);
+int hrt_ipc_close(void* ptr);
 
 /* Roofline probe of the hash-grid encode: useful GB/s (8 B per gather) of
  * independent random 8-byte gathers over this scene's hash table (F = 2),

@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("HRT_LIB", os.path.join(_HERE, "libhrt.so"))
 
 HRT_OK, HRT_EINVAL, HRT_ENONFINITE, HRT_ECUDA, HRT_ENOMEM = range(5)
 MODE_HYBRID, MODE_SURFACE, MODE_VOLUME = 0, 1, 2
+OUT_BY_PIXEL = 0x100
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 c_float_p = ctypes.POINTER(ctypes.c_float)
@@ -111,6 +112,11 @@ SIGNATURES = {
                                      ctypes.c_int32, vp, vp]),
     "hrt_set_rigid_base": (ctypes.c_int, [vp, vp, vp]),
     "hrt_refit_rigid": (ctypes.c_int, [vp, vp, ctypes.c_int32]),
+    "hrt_buffer_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(vp)]),
+    "hrt_buffer_free": (ctypes.c_int, [vp]),
+    "hrt_ipc_handle": (ctypes.c_int, [vp, vp]),
+    "hrt_ipc_open": (ctypes.c_int, [vp, ctypes.POINTER(vp)]),
+    "hrt_ipc_close": (ctypes.c_int, [vp]),
     "hrt_gather_peak": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
     "hrt_refit": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "hrt_field_sample": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, vp]),

@@ -1015,6 +1015,8 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
                const int32_t* pixels, int64_t n_pixels, double* out, hrt_stats* stats, void* stream) {
     if (!h || !cam) return fail(HRT_EINVAL, "null argument");
     if (spp < 1) return fail(HRT_EINVAL, "spp must be >= 1");
+    const int32_t by_pixel = (mode & HRT_OUT_BY_PIXEL) ? 1 : 0;
+    mode &= ~HRT_OUT_BY_PIXEL;
     if (mode < 0 || mode > 2) return fail(HRT_EINVAL, "bad mode");
     if (cam->width < 1 || cam->height < 1) return fail(HRT_EINVAL, "bad resolution");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1052,6 +1054,7 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
         a.out = out;
         a.out_offset = p0;
         a.tiled = (!pixels && kTiledFrame) ? 1 : 0;
+        a.out_by_pixel = by_pixel;
         a.trace = h->trace;
         a.trace_cap = h->trace_cap;
         pbeg(h, st);
@@ -1420,6 +1423,39 @@ int hrt_finalize(int32_t width, int32_t height, const double* src, const int32_t
     CK(cudaFreeAsync(bad, st));
     CK(cudaStreamSynchronize(st));
     if (nb) return fail(HRT_ENONFINITE, "finalize requires finite radiance");
+    return HRT_OK;
+}
+
+int hrt_buffer_alloc(int64_t bytes, void** ptr) {
+    if (!ptr || bytes <= 0) return fail(HRT_EINVAL, "bad arguments");
+    CK(cudaMalloc(ptr, (size_t)bytes));
+    return HRT_OK;
+}
+
+int hrt_buffer_free(void* ptr) {
+    if (ptr) CK(cudaFree(ptr));
+    return HRT_OK;
+}
+
+int hrt_ipc_handle(const void* ptr, uint8_t* handle64) {
+    if (!ptr || !handle64) return fail(HRT_EINVAL, "null argument");
+    cudaIpcMemHandle_t hd;
+    CK(cudaIpcGetMemHandle(&hd, const_cast<void*>(ptr)));
+    static_assert(sizeof(hd) == 64, "ipc handle size");
+    std::memcpy(handle64, &hd, 64);
+    return HRT_OK;
+}
+
+int hrt_ipc_open(const uint8_t* handle64, void** ptr) {
+    if (!ptr || !handle64) return fail(HRT_EINVAL, "null argument");
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, handle64, 64);
+    CK(cudaIpcOpenMemHandle(ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+    return HRT_OK;
+}
+
+int hrt_ipc_close(void* ptr) {
+    if (ptr) CK(cudaIpcCloseMemHandle(ptr));
     return HRT_OK;
 }
 

@@ -29,6 +29,7 @@ struct Args {
     double* out;             // (n_slots, 3) device output
     int64_t out_offset;      // slot offset in `out`
     int32_t tiled;           // full frame: slots walk 16x16 pixel tiles, out is raster
+    int32_t out_by_pixel;    // out is a raster frame indexed by global pixel id (may be a peer GPU's)
     int32_t* trace;          // optional (path, bounce, k, cell) records
     int64_t trace_cap;
 };
@@ -849,7 +850,9 @@ __global__ void k_accumulate(Args a) {
             acc[1] = acc[1] + s.Lg[p];
             acc[2] = acc[2] + s.Lb[p];
         }
-        double* o = a.out + 3 * (a.tiled ? slot_pixel(a, slot) : a.out_offset + slot);
+        // (out_by_pixel: a raster frame, possibly rank 0's mapped over NVLink - the
+        // frame "gather" is these stores, issued as each chunk's pixels finish)
+        double* o = a.out + 3 * ((a.tiled || a.out_by_pixel) ? slot_pixel(a, slot) : a.out_offset + slot);
         bool bad = false;
         for (int ch = 0; ch < 3; ++ch) {
             const double v = acc[ch] / (double)a.spp;

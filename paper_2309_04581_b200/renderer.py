@@ -65,21 +65,29 @@ class Renderer:
             pass
 
     # ------------------------------------------------------------ frames
-    def render_pixels(self, camera, spp, seed, mode=_lib.MODE_HYBRID, pixels=None, out=None):
+    def render_pixels(self, camera, spp, seed, mode=_lib.MODE_HYBRID, pixels=None, out=None,
+                      frame_ptr=None):
         """(n, 3) float64 device tensor for `pixels` (int32 device tensor of
-        pixel ids, None = whole frame in raster order)."""
+        pixel ids, None = whole frame in raster order). With `frame_ptr` (a
+        device address of a raster (w*h, 3) float64 frame, e.g. a peer GPU's
+        mapped with tiles.PeerFrame) the pixels are stored there by pixel id
+        instead (HRT_OUT_BY_PIXEL) and None is returned."""
         if spp < 1:
             raise ValueError("spp must be >= 1")
         cam = _lib.camera_desc(camera if isinstance(camera, dict) else pack_camera(camera))
         n = cam.width * cam.height if pixels is None else int(pixels.numel())
-        if out is None:
-            out = torch.empty((n, 3), dtype=torch.float64, device=self.device)
+        if frame_ptr is not None:
+            out_ptr, mode = ctypes.c_void_p(int(frame_ptr)), int(mode) | _lib.OUT_BY_PIXEL
+        else:
+            if out is None:
+                out = torch.empty((n, 3), dtype=torch.float64, device=self.device)
+            out_ptr = _dptr(out)
         if n == 0:                                   # a rank without tiles
             self.last_stats = _lib.Stats().as_dict()
             return out
         stats = _lib.Stats()
         rc = self.lib.hrt_render(self.handle, ctypes.byref(cam), int(spp), int(seed) & (2**64 - 1),
-                                 int(mode), _dptr(pixels), n, _dptr(out), ctypes.byref(stats),
+                                 int(mode), _dptr(pixels), n, out_ptr, ctypes.byref(stats),
                                  _stream())
         self.last_stats = stats.as_dict()
         _lib.check(rc, "hrt_render")

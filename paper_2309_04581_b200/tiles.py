@@ -80,3 +80,76 @@ class FrameGather:
             return None
         from .renderer import finalize_device
         return finalize_device(rows, self.w, self.h, hdr_output, pixel=self.row_pixel).cpu().numpy().tobytes()
+
+
+class _DeviceArray:
+    """__cuda_array_interface__ view of a raw device buffer (zero-copy torch.as_tensor)."""
+
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": tuple(shape),
+                                         "typestr": "<f8", "version": 3, "strides": None}
+
+
+class PeerFrame:
+    """Frame assembly over peer memory instead of a gather collective: rank 0
+    owns the raster (w*h, 3) float64 frame, every other rank maps it with CUDA
+    IPC (peer access over NVLink / NVSwitch), and each rank's accumulate kernel
+    stores its pixels straight into it (Renderer.render_pixels(...,
+    frame_ptr=pf.ptr)). `done()` (stream sync + barrier) makes rank 0's frame
+    complete; `finalize()` encodes it there (hrt_finalize). The process group
+    only carries the 64-byte handle and the barrier."""
+
+    def __init__(self, w, h, rank, world, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _lib
+        self.w, self.h, self.rank, self.world, self.group = w, h, rank, world, group
+        self.lib = _lib.load()
+        self._owner = rank == 0
+        p = ctypes.c_void_p()
+        if self._owner:
+            _lib.check(self.lib.hrt_buffer_alloc(w * h * 3 * 8, ctypes.byref(p)), "hrt_buffer_alloc")
+            hd = (ctypes.c_uint8 * 64)()
+            _lib.check(self.lib.hrt_ipc_handle(p, hd), "hrt_ipc_handle")
+            blob = [bytes(hd)]
+        else:
+            blob = [None]
+        if world > 1:
+            dist.broadcast_object_list(blob, src=0, group=group)
+        if not self._owner:
+            hd = (ctypes.c_uint8 * 64).from_buffer_copy(blob[0])
+            _lib.check(self.lib.hrt_ipc_open(hd, ctypes.byref(p)), "hrt_ipc_open")
+        self.ptr = p.value
+
+    def done(self):
+        import torch
+        import torch.distributed as dist
+        torch.cuda.current_stream().synchronize()
+        if self.world > 1:
+            dist.barrier(group=self.group)
+
+    def frame(self):
+        """Rank 0: the assembled (w*h, 3) frame as a zero-copy CUDA tensor."""
+        import torch
+        assert self._owner, "the frame lives on rank 0"
+        return torch.as_tensor(_DeviceArray(self.ptr, (self.w * self.h, 3)), device="cuda")
+
+    def finalize(self, hdr_output):
+        if not self._owner:
+            return None
+        from .renderer import finalize_device
+        return finalize_device(self.frame(), self.w, self.h, hdr_output).cpu().numpy().tobytes()
+
+    def close(self):
+        import torch.distributed as dist
+        if self.ptr is None:
+            return
+        if self.world > 1:
+            dist.barrier(group=self.group)        # no rank still writes into rank 0's frame
+        if self._owner:
+            self.lib.hrt_buffer_free(self.ptr)
+        else:
+            self.lib.hrt_ipc_close(self.ptr)
+        self.ptr = None
