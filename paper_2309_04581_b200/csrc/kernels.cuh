@@ -364,7 +364,7 @@ HRT_DEV int32_t gen_path(const Args& a, const MarchState& m, int32_t p, int32_t 
                 fws::SampleIn r;
                 r.x = p32.x; r.y = p32.y; r.z = p32.z; r.path = p;
                 m.in[(int64_t)cnt * nq + j] = r;
-                m.sk[(int64_t)cnt * nq + j] = k;
+                if (a.sc.em.n > 0 || a.trace) m.sk[(int64_t)cnt * nq + j] = k;   // read by shadows / trace only
                 ++cnt;
                 ++k;
             } else {
