@@ -292,9 +292,10 @@ HRT_DEV bool any_hit_w(const DevBvh& b, d3 o, d3 d, double t_min, double t_max) 
             if (leaf_any(b, w.r.y, o, d, t_min, t_max)) return true;
             h1 = false;
         }
-        if (h0 && h1) {
-            if (sp < kStack) stack[sp++] = w.r.y;
-            cur = w.r.x;
+        if (h0 && h1) {                  // nearer child first: occluders are found sooner
+            const bool near0 = n0 <= n1;
+            if (sp < kStack) stack[sp++] = near0 ? w.r.y : w.r.x;
+            cur = near0 ? w.r.x : w.r.y;
             continue;
         }
         if (h0 || h1) { cur = h0 ? w.r.x : w.r.y; continue; }

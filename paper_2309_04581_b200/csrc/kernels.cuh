@@ -577,6 +577,11 @@ __global__ void k_shadow(Args a, MarchState m, fws::RowMap rm, int64_t rows, int
 // and advance every lane one BVH node per iteration, so long traversals do
 // not hold the rest of the warp idle. Same culling and float64 triangle
 // tests as bvh::any_hit_w: the blocked / visible answer is identical.
+#ifndef HRT_SHADOW_ORDERED
+#define HRT_SHADOW_ORDERED 1
+#endif
+constexpr bool kShadowOrdered = HRT_SHADOW_ORDERED;
+
 __global__ void __launch_bounds__(256) k_shadow_trace(Args a, MarchState m) {
     const int32_t n = a.ps.counters[C_SHQ];
     int32_t* fetch = &a.ps.counters[C_SHF];
@@ -637,8 +642,9 @@ __global__ void __launch_bounds__(256) k_shadow_trace(Args a, MarchState m) {
         bool done = blocked;
         if (!done) {
             if (h0 && h1) {
-                if (sp < bvh::kStack) stack[sp++] = w.r.y;
-                cur = w.r.x;
+                const bool near0 = !kShadowOrdered || n0 <= n1;    // nearer child first
+                if (sp < bvh::kStack) stack[sp++] = near0 ? w.r.y : w.r.x;
+                cur = near0 ? w.r.x : w.r.y;
             } else if (h0 || h1) {
                 cur = h0 ? w.r.x : w.r.y;
             } else if (sp > 0) {
