@@ -14,7 +14,8 @@ namespace bvh {
 
 constexpr double BARY_EPS = 1e-7;
 constexpr double DET_EPS = 1e-12;
-constexpr int kStack = 64;   // the host builder caps the tree depth below this
+constexpr int kStack = 80;   // binary: <= 1 push per level; tree depth <= 32 + log2(faces) (+ log2(meshes) for a forest)
+constexpr int kStackQ = 128; // 4-wide: <= 3 pushes per level over <= ceil(depth / 2) levels
 
 // Reference surface.py:243-275 for one (ray, face) pair; +inf if rejected.
 HRT_DEV double moller_trumbore(d3 o, d3 d, const double* __restrict__ t9, double t_min,
@@ -305,14 +306,129 @@ HRT_DEV bool any_hit_w(const DevBvh& b, d3 o, d3 d, double t_min, double t_max) 
     return false;
 }
 
+// ---------------------------------------------------- 4-wide traversal
+HRT_DEV QNode load_q(const QNode* __restrict__ nodes, int32_t i) {
+    const float4* p = reinterpret_cast<const float4*>(nodes + i);
+    QNode q;
+    q.lox = __ldg(p); q.loy = __ldg(p + 1); q.loz = __ldg(p + 2);
+    q.hix = __ldg(p + 3); q.hiy = __ldg(p + 4); q.hiz = __ldg(p + 5);
+    q.ref = __ldg(reinterpret_cast<const int4*>(p + 6));
+    return q;
+}
+
+// Box tests of the 4 children; hit mask bit k, entry distance near[k].
+HRT_DEV uint32_t qchildren(const QNode& q, const Ray32& r, float t0, float t1, float near[4]) {
+    uint32_t m = 0;
+    const float lx[4] = {q.lox.x, q.lox.y, q.lox.z, q.lox.w}, ly[4] = {q.loy.x, q.loy.y, q.loy.z, q.loy.w};
+    const float lz[4] = {q.loz.x, q.loz.y, q.loz.z, q.loz.w}, hx[4] = {q.hix.x, q.hix.y, q.hix.z, q.hix.w};
+    const float hy[4] = {q.hiy.x, q.hiy.y, q.hiy.z, q.hiy.w}, hz[4] = {q.hiz.x, q.hiz.y, q.hiz.z, q.hiz.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (box32(lx[k], ly[k], lz[k], hx[k], hy[k], hz[k], r, t0, t1, near[k])) m |= 1u << k;
+    return m;
+}
+
+HRT_DEV int32_t qref(const QNode& q, int k) {
+    return k == 0 ? q.ref.x : (k == 1 ? q.ref.y : (k == 2 ? q.ref.z : q.ref.w));
+}
+
+// Nearest hit on the 4-wide tree (surface.py:377-440 contract).
+HRT_DEV int32_t closest_q(const DevBvh& b, d3 o, d3 d, double t_min, double t_max, double& best_t) {
+    best_t = INFINITY;
+    int32_t best_f = -1;
+    if (b.n_faces == 0) return -1;
+    const Ray32 r = prep32(o, d);
+    const float t0 = t_lo32(t_min);
+    int32_t stack[kStackQ];
+    float stack_t[kStackQ];
+    int sp = 0;
+    int32_t cur = 0;
+    while (true) {
+        const QNode q = load_q(b.qnodes, cur);
+        float nr[4];
+        uint32_t m = qchildren(q, r, t0, t_hi32(fmin(t_max, best_t)), nr);
+        // leaves first (they can only shrink best_t)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if ((m >> k & 1u) && qref(q, k) < 0) {
+                leaf_closest(b, qref(q, k), o, d, t_min, t_max, best_t, best_f);
+                m &= ~(1u << k);
+            }
+        // inner children: nearest next, the rest pushed far-to-near
+        const float lim = t_hi32(fmin(t_max, best_t));
+        int32_t next = -1;
+        while (m) {
+            int kb = -1;
+            float tb = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)              // farthest remaining first onto the stack
+                if ((m >> k & 1u) && nr[k] >= tb) { tb = nr[k]; kb = k; }
+            m &= ~(1u << kb);
+            if (tb > lim) continue;
+            if (m == 0) { next = qref(q, kb); break; }
+            if (sp < kStackQ) { stack[sp] = qref(q, kb); stack_t[sp] = tb; ++sp; }
+        }
+        if (next >= 0) { cur = next; continue; }
+        bool found = false;
+        const float lim2 = t_hi32(fmin(t_max, best_t));
+        while (sp > 0) {
+            --sp;
+            if (stack_t[sp] <= lim2) { cur = stack[sp]; found = true; break; }
+        }
+        if (!found) break;
+    }
+    return best_f;
+}
+
+// True if any face lies in (t_min, t_max] (surface.py:442-478), 4-wide tree.
+HRT_DEV bool any_hit_q(const DevBvh& b, d3 o, d3 d, double t_min, double t_max) {
+    if (b.n_faces == 0) return false;
+    const Ray32 r = prep32(o, d);
+    const float t0 = t_lo32(t_min), t1 = t_hi32(t_max);
+    int32_t stack[kStackQ];
+    int sp = 0;
+    int32_t cur = 0;
+    while (true) {
+        const QNode q = load_q(b.qnodes, cur);
+        float nr[4];
+        uint32_t m = qchildren(q, r, t0, t1, nr);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if ((m >> k & 1u) && qref(q, k) < 0) {
+                if (leaf_any(b, qref(q, k), o, d, t_min, t_max)) return true;
+                m &= ~(1u << k);
+            }
+        int32_t next = -1;
+        while (m) {
+            int kb = -1;
+            float tb = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if ((m >> k & 1u) && nr[k] >= tb) { tb = nr[k]; kb = k; }
+            m &= ~(1u << kb);
+            if (m == 0) { next = qref(q, kb); break; }
+            if (sp < kStackQ) stack[sp++] = qref(q, kb);
+        }
+        if (next >= 0) { cur = next; continue; }
+        if (sp == 0) break;
+        cur = stack[--sp];
+    }
+    return false;
+}
+
 #ifndef HRT_BVH64
 #define HRT_BVH64 0      // 1: traverse the float64 tree (reference-order culling)
 #endif
+#ifndef HRT_BVH_WIDTH
+#define HRT_BVH_WIDTH 4  // traversal tree: 4-wide QNodes (2: the binary WNode tree)
+#endif
 HRT_DEV int32_t nearest(const DevBvh& b, d3 o, d3 d, double t_min, double t_max, double& best_t) {
-    return HRT_BVH64 ? closest(b, o, d, t_min, t_max, best_t) : closest_w(b, o, d, t_min, t_max, best_t);
+    if (HRT_BVH64) return closest(b, o, d, t_min, t_max, best_t);
+    return HRT_BVH_WIDTH == 4 ? closest_q(b, o, d, t_min, t_max, best_t) : closest_w(b, o, d, t_min, t_max, best_t);
 }
 HRT_DEV bool occluded(const DevBvh& b, d3 o, d3 d, double t_min, double t_max) {
-    return HRT_BVH64 ? any_hit(b, o, d, t_min, t_max) : any_hit_w(b, o, d, t_min, t_max);
+    if (HRT_BVH64) return any_hit(b, o, d, t_min, t_max);
+    return HRT_BVH_WIDTH == 4 ? any_hit_q(b, o, d, t_min, t_max) : any_hit_w(b, o, d, t_min, t_max);
 }
 
 // WNode child boxes from the float64 tree after a refit (src: float64 node
@@ -463,6 +579,33 @@ __global__ void k_gather_faces(const double* __restrict__ src, int32_t n, const 
         const int32_t f = map[i];
         for (int k = 0; k < 3; ++k)
             for (int r = 0; r < 3; ++r) dst[k * b3 + 3 * (size_t)i + r] = src[k * n3 + 3 * (size_t)f + r];
+    }
+}
+
+// QNode child boxes from the float64 tree after a refit (src: float64 node per
+// slot, -1 = not from the tree: empty slot or a forest top-level slot).
+__global__ void k_qsync(QNode* q, const int4* __restrict__ src, const BvhNode* __restrict__ nodes,
+                        int32_t begin, int32_t n) {
+    for (int32_t i = begin + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int4 sidx = src[i];
+        const int32_t si[4] = {sidx.x, sidx.y, sidx.z, sidx.w};
+        float lo[4][3], hi[4][3];
+        for (int k = 0; k < 4; ++k) {
+            if (si[k] >= 0) {
+                BvhNode nb = nodes[si[k]];
+                wbox_dev(nb, lo[k], hi[k]);
+            }
+        }
+        QNode x = q[i];
+        float* f = reinterpret_cast<float*>(&x);       // lox[4] loy[4] loz[4] hix[4] hiy[4] hiz[4]
+        for (int k = 0; k < 4; ++k) {
+            if (si[k] < 0) continue;
+            for (int a = 0; a < 3; ++a) {
+                f[4 * a + k] = lo[k][a];
+                f[12 + 4 * a + k] = hi[k][a];
+            }
+        }
+        q[i] = x;
     }
 }
 

@@ -82,8 +82,17 @@ struct __align__(16) WNode {
     int4 r;     // ref0, ref1, -, -
 };
 
+// 4-wide traversal node (the binary WNode tree collapsed): 4 child boxes as
+// SoA float4s + refs (same ref encoding; empty slot: ref -1, far point box).
+struct __align__(16) QNode {
+    float4 lox, loy, loz, hix, hiy, hiz;
+    int4 ref;
+    int4 pad;
+};
+
 struct DevBvh {
-    const WNode* wnodes;    // float32-culling traversal tree (same leaves)
+    const QNode* qnodes;    // 4-wide float32-culling tree (traversal)
+    const WNode* wnodes;    // binary float32 tree (source of the 4-wide one)
     const BvhNode* nodes;
     const double* tri;      // leaf-ordered: v0, e1, e2 (9 doubles)
     const int32_t* tri_id;  // leaf order -> global face id

@@ -69,6 +69,9 @@ struct RefitState {              // device side of a BVH's GPU refit
     std::vector<int32_t> root_ref;   // and its WNode reference
     int32_t* d_roots = nullptr;
     double* d_rootbox = nullptr; // gathered root boxes (6 doubles each)
+    int4* qsrc = nullptr;        // float64 node behind each QNode child slot
+    int32_t n_q = 0, q_begin = 0;    // forest: QNodes [0, q_begin) hold the top level
+    std::vector<int32_t> qmap;   // WNode index -> QNode index of every tree root (forest)
     int32_t* parent = nullptr;
     int32_t* leaves = nullptr;
     int32_t* visits = nullptr;
@@ -174,6 +177,7 @@ int setup_refit(hrt_handle* h, const hrt::BvhHost& b, RefitState& r) {
 // refit the boxes bottom-up on the device.
 int refit_from_src(hrt_handle* h, const hrt::BvhHost& b, RefitState& r, DevBvh& dev);
 void build_tlas(const std::vector<hrt::BvhNodeHost>& box, const std::vector<int32_t>& ref, WNode* w);
+void collapse_top(const std::vector<WNode>& top, RefitState& r, std::vector<QNode>& Q);
 
 int refit_gpu(hrt_handle* h, const hrt::BvhHost& b, RefitState& r, DevBvh& dev, const double* v0,
               const double* e1, const double* e2) {
@@ -199,6 +203,9 @@ int refit_from_src(hrt_handle* h, const hrt::BvhHost& b, RefitState& r, DevBvh& 
     const unsigned g3 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((r.n_w + 255) / 256, 148 * 16));
     bvh::k_wsync<<<g3, 256>>>(const_cast<WNode*>(dev.wnodes), r.wsrc, dev.nodes, r.w_begin, r.n_w);
     CK(cudaGetLastError());
+    const unsigned g4 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((r.n_q + 255) / 256, 148 * 16));
+    bvh::k_qsync<<<g4, 256>>>(const_cast<QNode*>(dev.qnodes), r.qsrc, dev.nodes, r.q_begin, r.n_q);
+    CK(cudaGetLastError());
     if (!r.roots.empty()) {          // forest: new root boxes -> rebuild the top level
         const int32_t G = (int32_t)r.roots.size();
         bvh::k_root_boxes<<<(G + 255) / 256, 256>>>(dev.nodes, r.d_roots, G, r.d_rootbox);
@@ -214,6 +221,10 @@ int refit_from_src(hrt_handle* h, const hrt::BvhHost& b, RefitState& r, DevBvh& 
         std::vector<WNode> top(G - 1);
         build_tlas(boxes, r.root_ref, top.data());
         CK(cudaMemcpy(const_cast<WNode*>(dev.wnodes), top.data(), top.size() * sizeof(WNode),
+                      cudaMemcpyHostToDevice));
+        std::vector<QNode> qtop;
+        collapse_top(top, r, qtop);
+        CK(cudaMemcpy(const_cast<QNode*>(dev.qnodes), qtop.data(), qtop.size() * sizeof(QNode),
                       cudaMemcpyHostToDevice));
     }
     return HRT_OK;
@@ -290,6 +301,124 @@ void build_tlas(const std::vector<hrt::BvhNodeHost>& box, const std::vector<int3
     rec(0, (int32_t)box.size());
 }
 
+// ---- 4-wide traversal tree: the binary WNode tree collapsed (each QNode
+// takes a WNode's two children and expands inner ones, largest area first,
+// until it has 4 slots). Boxes are copied, so culling stays conservative.
+struct QSlot {
+    float lo[3], hi[3];
+    int32_t ref, src;
+};
+
+QSlot wslot(const WNode& w, const int2& s, int k) {
+    QSlot q;
+    if (k == 0) {
+        q.lo[0] = w.a.x; q.lo[1] = w.a.y; q.lo[2] = w.a.z;
+        q.hi[0] = w.a.w; q.hi[1] = w.b.x; q.hi[2] = w.b.y;
+        q.ref = w.r.x; q.src = s.x;
+    } else {
+        q.lo[0] = w.b.z; q.lo[1] = w.b.w; q.lo[2] = w.c.x;
+        q.hi[0] = w.c.y; q.hi[1] = w.c.z; q.hi[2] = w.c.w;
+        q.ref = w.r.y; q.src = s.y;
+    }
+    return q;
+}
+
+double qarea(const QSlot& q) {
+    double e[3];
+    for (int a = 0; a < 3; ++a) e[a] = std::max(0.0, (double)q.hi[a] - (double)q.lo[a]);
+    return e[0] * e[1] + e[1] * e[2] + e[2] * e[0];
+}
+
+// Collapse WNode w into QNode index `at` (already reserved); children that
+// `expand` accepts are collapsed recursively into indices taken from *next,
+// other inner refs are translated with `map_inner`.
+void qcollapse(const WNode* W, const int2* S, int32_t w, int32_t at, std::vector<QNode>& Q,
+               std::vector<int4>& QS, int32_t* next, const std::function<bool(int32_t)>& expand,
+               const std::function<int32_t(int32_t)>& map_inner) {
+    std::vector<QSlot> sl = {wslot(W[w], S[w], 0), wslot(W[w], S[w], 1)};
+    while (sl.size() < 4) {
+        int best = -1;
+        double ba = -1.0;
+        for (size_t k = 0; k < sl.size(); ++k)
+            if (sl[k].ref >= 0 && expand(sl[k].ref) && qarea(sl[k]) > ba) { ba = qarea(sl[k]); best = (int)k; }
+        if (best < 0) break;
+        const int32_t c = sl[best].ref;
+        sl[best] = wslot(W[c], S[c], 0);
+        sl.push_back(wslot(W[c], S[c], 1));
+    }
+    QNode q;
+    float* f = reinterpret_cast<float*>(&q);
+    int32_t refs[4] = {-1, -1, -1, -1}, srcs[4] = {-1, -1, -1, -1};
+    for (int k = 0; k < 4; ++k)
+        for (int a = 0; a < 3; ++a) { f[4 * a + k] = 1e30f; f[12 + 4 * a + k] = 1e30f; }
+    std::vector<std::pair<int32_t, int32_t>> todo;       // (wnode, qnode) to collapse after this one
+    for (size_t k = 0; k < sl.size(); ++k) {
+        for (int a = 0; a < 3; ++a) { f[4 * a + k] = sl[k].lo[a]; f[12 + 4 * a + k] = sl[k].hi[a]; }
+        srcs[k] = sl[k].src;
+        if (sl[k].ref < 0) {
+            refs[k] = sl[k].ref;
+        } else if (expand(sl[k].ref)) {
+            refs[k] = (*next)++;
+            todo.push_back({sl[k].ref, refs[k]});
+        } else {
+            refs[k] = map_inner(sl[k].ref);
+        }
+    }
+    q.ref = make_int4(refs[0], refs[1], refs[2], refs[3]);
+    q.pad = make_int4(0, 0, 0, 0);
+    if ((int32_t)Q.size() <= at) { Q.resize(at + 1); QS.resize(at + 1); }
+    Q[at] = q;
+    QS[at] = make_int4(srcs[0], srcs[1], srcs[2], srcs[3]);
+    for (auto& t : todo) qcollapse(W, S, t.first, t.second, Q, QS, next, expand, map_inner);
+}
+
+// 4-wide tree of a built WNode array (single tree or forest), r.qmap / q_begin set.
+void build_qnodes(const std::vector<WNode>& W, const std::vector<int2>& S, RefitState& r,
+                  std::vector<QNode>& Q, std::vector<int4>& QS) {
+    Q.clear();
+    QS.clear();
+    r.qmap.clear();
+    const int32_t T = r.w_begin;
+    if (r.roots.empty() || T == 0) {                   // one tree
+        int32_t next = 1;
+        qcollapse(W.data(), S.data(), 0, 0, Q, QS, &next, [](int32_t) { return true; },
+                  [](int32_t c) { return c; });
+        r.q_begin = 0;
+        return;
+    }
+    // forest: trees first (from index T), then the top level into [0, T)
+    r.qmap.assign(W.size(), -1);
+    int32_t next = T;
+    Q.resize(T);
+    QS.assign(T, make_int4(-1, -1, -1, -1));
+    for (int32_t rf : r.root_ref) {
+        if (rf < 0) continue;                         // tree of one leaf: stays a leaf ref
+        const int32_t at = next++;
+        r.qmap[rf] = at;
+        qcollapse(W.data(), S.data(), rf, at, Q, QS, &next, [T](int32_t c) { return c >= T; },
+                  [](int32_t c) { return c; });
+    }
+    r.q_begin = T;
+    int32_t top = 1;
+    std::vector<int32_t>& qm = r.qmap;
+    qcollapse(W.data(), S.data(), 0, 0, Q, QS, &top, [T](int32_t c) { return c < T; },
+              [&qm](int32_t c) { return qm[c]; });
+    for (int32_t i = 0; i < T; ++i) QS[i] = make_int4(-1, -1, -1, -1);   // top level: host-rebuilt
+}
+
+// Per-frame top level of a forest in QNodes [0, q_begin): collapse the
+// rebuilt binary top level, tree roots mapped through qmap.
+void collapse_top(const std::vector<WNode>& top, RefitState& r, std::vector<QNode>& Q) {
+    const int32_t T = r.w_begin;
+    std::vector<int2> S(T, make_int2(-1, -1));
+    std::vector<int4> QS;
+    Q.clear();
+    int32_t next = 1;
+    std::vector<int32_t>& qm = r.qmap;
+    qcollapse(top.data(), S.data(), 0, 0, Q, QS, &next, [T](int32_t c) { return c < T; },
+              [&qm](int32_t c) { return qm[c]; });
+}
+
 // float32-culling tree over the same leaves: one WNode per inner float64
 // node (a root leaf gets a WNode with an empty second child); src records
 // the float64 node behind each child slot for k_wsync after refits. A
@@ -336,7 +465,7 @@ void build_wnodes(const hrt::BvhHost& b, std::vector<WNode>& w, std::vector<int2
 
 int upload_bvh(hrt_handle* h, const hrt::BvhHost& b, DevBvh& out, RefitState& r) {
     out.n_faces = b.n_faces;
-    out.nodes = nullptr; out.tri = nullptr; out.tri_id = nullptr; out.wnodes = nullptr;
+    out.nodes = nullptr; out.tri = nullptr; out.tri_id = nullptr; out.wnodes = nullptr; out.qnodes = nullptr;
     r.wsrc = nullptr;
     r.n_w = 0;
     if (b.n_faces == 0) return HRT_OK;
@@ -350,6 +479,14 @@ int upload_bvh(hrt_handle* h, const hrt::BvhHost& b, DevBvh& out, RefitState& r)
         if ((rc = h->upload(src.data(), src.size(), &r.wsrc))) return rc;
         out.wnodes = dw;
         r.n_w = (int32_t)w.size();
+        std::vector<QNode> q;
+        std::vector<int4> qs;
+        build_qnodes(w, src, r, q, qs);
+        QNode* dq;
+        if ((rc = h->upload(q.data(), q.size(), &dq))) return rc;
+        if ((rc = h->upload(qs.data(), qs.size(), &r.qsrc))) return rc;
+        out.qnodes = dq;
+        r.n_q = (int32_t)q.size();
         if (!r.roots.empty()) {
             if ((rc = h->upload(r.roots.data(), r.roots.size(), &r.d_roots))) return rc;
             if ((rc = h->alloc(r.roots.size() * 6 * 8, reinterpret_cast<void**>(&r.d_rootbox)))) return rc;
@@ -1098,6 +1235,10 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
         stats->launches = h->launches;
         for (int i = 0; i < 8; ++i) stats->stage_ms[i] = (float)h->stage_ms[i];
         stats->batch_rows = h->batch_rows + (int64_t)tot[S_ROWS];
+#ifdef HRT_COUNT_STEPS
+        fprintf(stderr, "shadow trace: node steps %llu  triangle tests %llu  blocked %llu  queued %s\n",
+                tot[5], tot[6], tot[7], "");
+#endif
     }
     if (ctr[C_NONFINITE] != 0) return fail(HRT_ENONFINITE, "non-finite or negative radiance in frame");
     return HRT_OK;

@@ -581,6 +581,10 @@ __global__ void k_shadow(Args a, MarchState m, fws::RowMap rm, int64_t rows, int
 #define HRT_SHADOW_ORDERED 1
 #endif
 constexpr bool kShadowOrdered = HRT_SHADOW_ORDERED;
+#ifndef HRT_REFILL_LANES
+#define HRT_REFILL_LANES 8
+#endif
+constexpr int kRefillLanes = HRT_REFILL_LANES;    // idle lanes that trigger a warp refill
 
 __global__ void __launch_bounds__(256) k_shadow_trace(Args a, MarchState m) {
     const int32_t n = a.ps.counters[C_SHQ];
@@ -594,14 +598,17 @@ __global__ void __launch_bounds__(256) k_shadow_trace(Args a, MarchState m) {
     double tmax = 0.0;
     bvh::Ray32 r32{};
     float t0 = 0.f, t1 = 0.f;
-    int32_t stack[bvh::kStack];
+    int32_t stack[bvh::kStackQ];
     int sp = 0;
     int32_t cur = 0, row = 0, idx = 0;
+#ifdef HRT_COUNT_STEPS
+    long long n_steps = 0, n_mt = 0, n_blocked = 0;
+#endif
     while (true) {
         const bool idle = qi < 0 && !exhausted;
         const uint32_t need = __ballot_sync(0xffffffffu, idle);
         const uint32_t busy = __ballot_sync(0xffffffffu, qi >= 0);
-        if (need && (__popc(need) >= 8 || busy == 0)) {
+        if (need && (__popc(need) >= kRefillLanes || busy == 0)) {
             const int leader = __ffs(need) - 1;
             int32_t base = 0;
             if ((int)lane == leader) base = atomicAdd(fetch, __popc(need));
@@ -628,12 +635,51 @@ __global__ void __launch_bounds__(256) k_shadow_trace(Args a, MarchState m) {
         }
         if (__all_sync(0xffffffffu, exhausted || qi < 0) && __all_sync(0xffffffffu, exhausted)) break;
         if (qi < 0) continue;
+        if (HRT_BVH_WIDTH == 4) {
+            // one step of bvh::any_hit_q: either one 4-wide node (hit children pushed
+            // far to near, the nearest taken next) or one leaf triangle, so a warp's
+            // lanes never serialise several triangle tests behind one node test
+            bool blocked = false, done = false;
+            if (cur < 0) {
+                blocked = bvh::leaf_any(b, cur, o, d, t_min, tmax);
+                done = blocked;
+            } else {
+                const QNode qn = bvh::load_q(b.qnodes, cur);
+                float nr[4];
+                uint32_t mk4 = bvh::qchildren(qn, r32, t0, t1, nr);
+                while (mk4) {
+                    int kb = -1;
+                    float tb = -INFINITY;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if ((mk4 >> k & 1u) && nr[k] >= tb) { tb = nr[k]; kb = k; }
+                    mk4 &= ~(1u << kb);
+                    if (sp < bvh::kStackQ) stack[sp++] = bvh::qref(qn, kb);
+                }
+            }
+#ifdef HRT_COUNT_STEPS
+            ++n_steps;
+#endif
+            if (!done) {
+                if (sp > 0) cur = stack[--sp];
+                else done = true;
+            }
+            if (done) {
+                m.shadow[row] = blocked ? idx + 1 : 0;
+                qi = -1;
+            }
+            continue;
+        }
         // one node of the traversal (bvh::any_hit_w, unrolled into steps)
         const WNode w = bvh::load_w(b.wnodes, cur);
         bool h0, h1;
         float n0, n1;
         bvh::wchildren(w, r32, t0, t1, h0, h1, n0, n1);
         bool blocked = false;
+#ifdef HRT_COUNT_STEPS
+        ++n_steps;
+        n_mt += (h0 && w.r.x < 0) + (h1 && w.r.y < 0);
+#endif
         if (h0 && w.r.x < 0) { blocked = bvh::leaf_any(b, w.r.x, o, d, t_min, tmax); h0 = false; }
         if (!blocked && h1 && w.r.y < 0) {
             blocked = bvh::leaf_any(b, w.r.y, o, d, t_min, tmax);
@@ -656,8 +702,16 @@ __global__ void __launch_bounds__(256) k_shadow_trace(Args a, MarchState m) {
         if (done) {
             m.shadow[row] = blocked ? idx + 1 : 0;
             qi = -1;
+#ifdef HRT_COUNT_STEPS
+            n_blocked += blocked;
+#endif
         }
     }
+#ifdef HRT_COUNT_STEPS
+    stat_add(a.ps.stats, 5, n_steps);
+    stat_add(a.ps.stats, 6, n_mt);
+    stat_add(a.ps.stats, 7, n_blocked);
+#endif
 }
 
 // Device-driven march round (no host sync): flip to the queue k_step will
