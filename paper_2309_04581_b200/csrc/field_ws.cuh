@@ -81,10 +81,24 @@ struct __align__(16) SampleIn {
 struct RowMap {
     int64_t stride;
     int32_t width;
+    uint32_t magic;         // l / width == (l * magic) >> shift for l < 2^31 (set_rows)
+    uint32_t shift;
 };
+// Device-driven rounds set the map from the round counters: the division by
+// `width` becomes one wide multiply + shift (magic = ceil(2^s / width),
+// s = 31 + ceil(log2 width); exact for l < 2^31 since l * (magic * width -
+// 2^s) < 2^31 * width <= 2^s).
+__device__ __forceinline__ void set_rows(RowMap& m, int32_t width, int64_t stride) {
+    m.width = width;
+    m.stride = stride;
+    if (width <= 0) return;
+    const uint32_t lg = width > 1 ? 32u - (uint32_t)__clz(width - 1) : 0u;
+    m.shift = 31u + lg;
+    m.magic = (uint32_t)(((1ull << m.shift) + (uint64_t)width - 1) / (uint64_t)width);
+}
 __device__ __forceinline__ int64_t phys_row(const RowMap& m, int64_t l) {
     if (m.width == 0) return l;
-    const uint32_t i = (uint32_t)l / (uint32_t)m.width;      // batches stay below 2^31 rows
+    const uint32_t i = (uint32_t)(((uint64_t)(uint32_t)l * m.magic) >> m.shift);   // l / width
     return (int64_t)i * m.stride + (int64_t)((uint32_t)l - i * (uint32_t)m.width);
 }
 
@@ -149,8 +163,7 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
     constexpr uint32_t kStageCols = E / 2;
     const int warp = threadIdx.x >> 5;
     if (round_ctr) {                 // device-driven march round (kern::k_round_begin counters)
-        rmap.width = round_ctr[C_MQ0 + (round_ctr[C_CUR] ^ 1)];
-        rmap.stride = round_ctr[C_STRIDE];
+        set_rows(rmap, round_ctr[C_MQ0 + (round_ctr[C_CUR] ^ 1)], round_ctr[C_STRIDE]);
         n = (int64_t)rmap.width * round_ctr[C_S];
         if (blockIdx.x == 0 && threadIdx.x == 0 && stats) atomicAdd(stats + S_ROWS, (unsigned long long)n);
     }

@@ -677,7 +677,7 @@ int field_eval(hrt_handle* h, const double* p, const double* d, int64_t n, float
                                                static_cast<fws::SampleIn*>(in),
                                                static_cast<float4*>(dir), e);
     CK(cudaGetLastError());
-    int rc = field_ws(h, static_cast<fws::SampleIn*>(in), fws::RowMap{0, 0}, n, static_cast<float4*>(dir),
+    int rc = field_ws(h, static_cast<fws::SampleIn*>(in), fws::RowMap{}, n, static_cast<float4*>(dir),
                       static_cast<float4*>(res), density_only, st);
     if (rc == HRT_OK) {
         kern::k_field_post<<<g, kThreads, 0, st>>>(static_cast<float4*>(res), e, n, sigma,
@@ -750,6 +750,7 @@ int ensure_state(hrt_handle* h, int64_t paths) {
         m.mq[0] = take_i(); m.mq[1] = take_i();
         m.dir32 = reinterpret_cast<float4*>(take(f4));
         m.h4 = reinterpret_cast<uint64_t*>(take(dbl));
+        m.bounce = take_i();
         m.in = reinterpret_cast<fws::SampleIn*>(take((size_t)nb * 16));
         m.sk = reinterpret_cast<int32_t*>(take((size_t)nb * 4));
         m.out = reinterpret_cast<float4*>(take((size_t)nb * 16));
@@ -833,6 +834,10 @@ constexpr int64_t kMaxRoundSamples = 256;      // (k_round_begin uses the same 2
 #define HRT_ROUNDS_PER_CHECK 2
 #endif
 constexpr int kRoundsPerCheck = HRT_ROUNDS_PER_CHECK;
+#ifndef HRT_MIXED_MARCH
+#define HRT_MIXED_MARCH 1
+#endif
+constexpr bool kMixedMarch = HRT_MIXED_MARCH;     // continuous wavefront march (kern::advance)
 int32_t round_samples(const hrt_handle* h, int64_t live) {
     int64_t S = kern::kRoundSamples;
     if (kTailTiles > 0) {
@@ -905,17 +910,18 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
             for (int k = 0; k < kRoundsPerCheck; ++k) {
                 pbeg(h, st);
                 kern::k_round_begin<<<1, 1, 0, st>>>(h->ps.counters, h->ps.stats, target, cap);
-                kern::k_step<<<g, kThreads, 0, st>>>(a, h->ms);
+                if (a.mixed) kern::k_step<true><<<g, kThreads, 0, st>>>(a, h->ms);
+                else kern::k_step<false><<<g, kThreads, 0, st>>>(a, h->ms);
                 CK(cudaGetLastError());
                 pend(h, HRT_STAGE_COMPOSITE, st);
                 pbeg(h, st);
-                if ((rc = field_ws(h, h->ms.in, fws::RowMap{0, 0}, 0, h->ms.dir32, h->ms.out, 0, st,
+                if ((rc = field_ws(h, h->ms.in, fws::RowMap{}, 0, h->ms.dir32, h->ms.out, 0, st,
                                    h->ps.counters)))
                     return rc;
                 pend(h, HRT_STAGE_FIELD, st);
                 if (h->sc.em.n > 0) {
                     pbeg(h, st);
-                    kern::k_shadow<<<gsh, kThreads, 0, st>>>(a, h->ms, fws::RowMap{0, 0}, 0, 1);
+                    kern::k_shadow<<<gsh, kThreads, 0, st>>>(a, h->ms, fws::RowMap{}, 0, 1);
                     CK(cudaGetLastError());
                     if ((rc = shadow_trace(h, a, st))) return rc;
                     pend(h, HRT_STAGE_SHADOW, st);
@@ -948,14 +954,14 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
         CK(cudaGetLastError());
         pend(h, HRT_STAGE_MARCH_GEN, st);
         pbeg(h, st);
-        if ((rc = field_ws(h, h->ms.in, fws::RowMap{0, 0}, (int64_t)live * S, h->ms.dir32, h->ms.out, 0,
+        if ((rc = field_ws(h, h->ms.in, fws::RowMap{}, (int64_t)live * S, h->ms.dir32, h->ms.out, 0,
                            st)))
             return rc;
         pend(h, HRT_STAGE_FIELD, st);
         if (h->sc.em.n > 0) {
             const int64_t rows = (int64_t)live * S;
             pbeg(h, st);
-            kern::k_shadow<<<grid_for(h, rows), kThreads, 0, st>>>(a, h->ms, fws::RowMap{0, 0}, rows, 0);
+            kern::k_shadow<<<grid_for(h, rows), kThreads, 0, st>>>(a, h->ms, fws::RowMap{}, rows, 0);
             CK(cudaGetLastError());
             if ((rc = shadow_trace(h, a, st))) return rc;
             pend(h, HRT_STAGE_SHADOW, st);
@@ -1000,6 +1006,21 @@ int run_bounces(hrt_handle* h, kern::Args& a, int64_t paths, int mode, cudaStrea
         ++h->launches;
         if (field && (rc = march(h, a, paths, st))) return rc;
         return HRT_OK;
+    }
+    if (kMixedMarch && field && mode == HRT_MODE_HYBRID && !a.trace &&
+        h->sc.field.kind == HRT_FIELD_NEURAL && h->sc.n_bounces >= 1) {
+        // continuous wavefront march: bounce 1's rays are intersected here,
+        // every later bounce inside the march rounds (kern::advance)
+        a.bounce = 1;
+        a.cur = 0;
+        a.mixed = 1;
+        pbeg(h, st);
+        kern::k_reset_queue<<<1, 1, 0, st>>>(h->ps.counters, 1);
+        kern::k_intersect<<<g, kThreads, 0, st>>>(a);
+        CK(cudaGetLastError());
+        pend(h, HRT_STAGE_INTERSECT, st);
+        h->launches += 2;
+        return march_neural(h, a, paths, st);
     }
     for (int b = 1; b <= h->sc.n_bounces; ++b) {
         a.bounce = b;

@@ -32,6 +32,7 @@ struct Args {
     int32_t out_by_pixel;    // out is a raster frame indexed by global pixel id (may be a peer GPU's)
     int32_t* trace;          // optional (path, bounce, k, cell) records
     int64_t trace_cap;
+    int32_t mixed;           // continuous wavefront march: bounces advance inside k_step
 };
 
 // One of a two-entry pointer array in a kernel parameter. A plain
@@ -308,6 +309,7 @@ struct MarchState {         // per path, valid while the path is marching
     int32_t* shadow;        // per batch sample: 0 visible / 1 + blocked emitter index
     struct QRay* shq;       // shadow rays that reach the blocker tree (k_shadow_trace)
     uint64_t* h4;           // per path: rng::prefix(seed, pix, smp, bounce) of this bounce
+    int32_t* bounce;        // per path: its current bounce (continuous wavefront march)
 };
 
 // A queued shadow ray (64 B): origin = the NeRF sample point, float64 as the
@@ -317,23 +319,79 @@ struct __align__(16) QRay {
     int32_t row, idx;
 };
 
+// K8 for one path at its hit of bounce `bounce` (render.py:221-244): normal
+// flip, emission with the post-march throughput, BSDF sample, throughput,
+// spawn. Returns true if the path goes on (hit and max(T_spec) >= threshold).
+HRT_DEV bool shade_one(const Args& a, int32_t p, int32_t bounce, Acc& c) {
+    const PathState& s = a.ps;
+    const DevScene& sc = a.sc;
+    const int32_t f = s.face[p];
+    if (f < 0) return false;
+    const double t = s.t_hit[p];
+    const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+    const d3 point = {o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
+    const d3 n_raw = mk(sc.normal[3 * f], sc.normal[3 * f + 1], sc.normal[3 * f + 2]);
+    const bool facing = dot(n_raw, d) < 0.0;
+    const d3 nrm = facing ? n_raw : neg(n_raw);
+    if (facing) {
+        c.L[0] = c.L[0] + c.Ts[0] * sc.emission[3 * f];
+        c.L[1] = c.L[1] + c.Ts[1] * sc.emission[3 * f + 1];
+        c.L[2] = c.L[2] + c.Ts[2] * sc.emission[3 * f + 2];
+    }
+    const int32_t mi = sc.mesh_of[f];
+    const int32_t kind = sc.mat.kind[mi];
+    const d3 wo = neg(d);
+    const int32_t pix = s.pix[p], smp = s.smp[p];
+    d3 nd;
+    if (kind == 0) {
+        const double u1 = rng::uniform(a.seed, pix, smp, bounce, rng::BSDF_U, 0);
+        const double u2 = rng::uniform(a.seed, pix, smp, bounce, rng::BSDF_V, 0);
+        nd = path::cosine_sample(nrm, u1, u2);
+    } else if (kind == 1) {
+        nd = path::reflect(wo, nrm);
+    } else {
+        const double u = rng::uniform(a.seed, pix, smp, bounce, rng::BSDF_LOBE, 0);
+        nd = path::dielectric_sample(wo, nrm, facing, sc.mat.ior[mi], sc.mat.r0[mi], u);
+    }
+    for (int ch = 0; ch < 3; ++ch) c.Ts[ch] = c.Ts[ch] * sc.mat.rgb[3 * mi + ch];
+    s.ox[p] = point.x + sc.spawn_eps * nd.x;
+    s.oy[p] = point.y + sc.spawn_eps * nd.y;
+    s.oz[p] = point.z + sc.spawn_eps * nd.z;
+    s.dx[p] = nd.x; s.dy[p] = nd.y; s.dz[p] = nd.z;
+    return fmax(fmax(c.Ts[0], c.Ts[1]), c.Ts[2]) >= sc.threshold;
+}
+
+// Segment set-up of path p for the march of bounce `bounce`; false (n = 0)
+// when the ray has no segment inside the field box before its hit.
+HRT_DEV bool seg_one(const Args& a, const MarchState& m, int32_t p, int32_t bounce) {
+    const PathState& s = a.ps;
+    const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+    Segment g;
+    if (!segment(a.sc, o, d, s.t_hit[p], g)) {
+        m.n[p] = 0;
+        m.k[p] = 0;
+        return false;
+    }
+    m.s0[p] = g.s0;
+    m.delta[p] = g.delta;
+    m.n[p] = g.n;
+    m.k[p] = 0;
+    const d3 df = field_dir(a.sc.field, d);
+    m.dir32[p] = make_float4((float)df.x, (float)df.y, (float)df.z, 0.f);
+    if (m.shq) m.h4[p] = rng::prefix(a.seed, s.pix[p], s.smp[p], bounce);
+    return true;
+}
+
+// Paths with a segment enter march queue 0; with a.mixed every path does
+// (k_step then shades and advances those without one).
 __global__ void k_seg(Args a, MarchState m) {
     const int32_t n = a.ps.counters[a.cur];
     const int32_t* q = pick(a.ps.queue, a.cur);
-    const PathState& s = a.ps;
     for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
         const int32_t p = q[j];
-        const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
-        Segment g;
-        if (!segment(a.sc, o, d, s.t_hit[p], g)) continue;
-        m.s0[p] = g.s0;
-        m.delta[p] = g.delta;
-        m.n[p] = g.n;
-        m.k[p] = 0;
-        const d3 df = field_dir(a.sc.field, d);
-        m.dir32[p] = make_float4((float)df.x, (float)df.y, (float)df.z, 0.f);
-        if (m.shq) m.h4[p] = rng::prefix(a.seed, s.pix[p], s.smp[p], a.bounce);
-        m.mq[0][reserve(&a.ps.counters[C_MQ0])] = p;
+        const bool has = seg_one(a, m, p, a.bounce);
+        if (a.mixed) m.bounce[p] = a.bounce;
+        if (has || a.mixed) m.mq[0][reserve(&a.ps.counters[C_MQ0])] = p;
     }
 }
 
@@ -483,9 +541,37 @@ __global__ void __launch_bounds__(256, HRT_COMP_MINB) k_comp(Args a, MarchState 
 // generates its next samples at rows i * nq + r. One pass over the path
 // state per round instead of two (k_gen + k_comp); a path whose remaining
 // candidates are all empty cells keeps a rank with S hole rows.
+// Continuous wavefront march (a.mixed): a path whose segment is over is
+// shaded at its hit (shade_one), and if it goes on, its next bounce's ray is
+// intersected (K2) and its segment set up here, inside the round, so its
+// samples join the same batch as the other paths' instead of waiting for a
+// per-bounce tail of small rounds. Every path still runs the reference's
+// per-path sequence (march b -> shade b -> intersect b+1 -> march b+1 ...)
+// with the same arithmetic, so results are bit-identical to the per-bounce
+// loop. Returns true when the path has a segment to march.
+HRT_DEV bool advance(const Args& a, const MarchState& m, int32_t p, Acc& c, int32_t& segs) {
+    const PathState& s = a.ps;
+    int32_t b = m.bounce[p];
+    while (true) {
+        if (!shade_one(a, p, b, c)) return false;
+        if (b >= a.sc.n_bounces) return false;
+        ++b;
+        m.bounce[p] = b;
+        double t = INFINITY;
+        const int32_t f = bvh::nearest(a.sc.bvh, mk(s.ox[p], s.oy[p], s.oz[p]), mk(s.dx[p], s.dy[p], s.dz[p]),
+                                       0.0, INFINITY, t);
+        s.t_hit[p] = t;
+        s.face[p] = f;
+        ++segs;
+        if (seg_one(a, m, p, b) && !halted(a.sc, c)) return true;
+        // nothing to march on this bounce (no segment, or halted): its hit next
+    }
+}
+
 #ifndef HRT_STEP_MINB
 #define HRT_STEP_MINB 3
 #endif
+template <bool kMixed>
 __global__ void __launch_bounds__(256, HRT_STEP_MINB) k_step(Args a, MarchState m) {
     const int32_t* ctr = a.ps.counters;
     const int32_t mcur = ctr[C_CUR], S = ctr[C_S], prev_nq = ctr[C_PSTRIDE], first = ctr[C_FIRST];
@@ -494,7 +580,7 @@ __global__ void __launch_bounds__(256, HRT_STEP_MINB) k_step(Args a, MarchState 
     int32_t* next = pick(m.mq, mcur ^ 1);
     int32_t* next_n = &a.ps.counters[C_MQ0 + (mcur ^ 1)];
     const PathState& s = a.ps;
-    int32_t done = 0, made = 0;
+    int32_t done = 0, made = 0, held = 0, segs = 0;
     for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += gridDim.x * blockDim.x) {
         const int32_t p = q[j];
         Acc c;
@@ -503,9 +589,12 @@ __global__ void __launch_bounds__(256, HRT_STEP_MINB) k_step(Args a, MarchState 
         if (!first) {
             const bool stop = comp_path<false>(a, m, p, m.base[p], prev_nq, m.cnt[p], m.delta[p], c,
                                                done);
-            store_acc(s, p, c);
             go = !stop && !halted(a.sc, c) && m.k[p] < m.n[p];
+        } else if (kMixed) {
+            go = m.k[p] < m.n[p];
         }
+        if (kMixed && !go) go = advance(a, m, p, c, segs);
+        if (!first || kMixed) store_acc(s, p, c);
         if (go) {
             // dense next batch: rank r among the paths that go on; rows
             // i * nq + r (the field engine reads them through a RowMap)
@@ -513,11 +602,15 @@ __global__ void __launch_bounds__(256, HRT_STEP_MINB) k_step(Args a, MarchState 
             next[r] = p;
             m.base[p] = r;
             made += gen_path(a, m, p, r, nq, S, c);
+            ++held;
         }
     }
     warp_stat_add(a.ps.stats, S_SAMPLES, done);
     warp_stat_add(a.ps.stats, S_EVALS, made);
-    const int32_t any = __reduce_add_sync(0xffffffffu, made);
+    if (kMixed) warp_stat_add(a.ps.stats, S_SEGMENTS, segs);
+    // the host stops the rounds when a round's C_NS is 0: samples made, or
+    // (continuous march) paths still holding a rank
+    const int32_t any = __reduce_add_sync(0xffffffffu, kMixed ? made + held : made);
     if ((threadIdx.x & 31) == 0 && any) atomicAdd(&a.ps.counters[C_NS], any);
 }
 
@@ -529,8 +622,7 @@ __global__ void k_shadow(Args a, MarchState m, fws::RowMap rm, int64_t rows, int
     const PathState& s = a.ps;
     if (dev_rows) {                  // device-driven round: this round's batch shape
         const int32_t* ctr = a.ps.counters;
-        rm.width = ctr[C_MQ0 + (ctr[C_CUR] ^ 1)];
-        rm.stride = ctr[C_STRIDE];
+        fws::set_rows(rm, ctr[C_MQ0 + (ctr[C_CUR] ^ 1)], ctr[C_STRIDE]);
         rows = (int64_t)rm.width * ctr[C_S];
     }
     int32_t cast = 0;
@@ -563,7 +655,7 @@ __global__ void k_shadow(Args a, MarchState m, fws::RowMap rm, int64_t rows, int
                     code = -1;                         // decided by k_shadow_trace
                 }
             } else {
-                code = path::shadow_code(a.sc, x, a.seed, s.pix[p], s.smp[p], a.bounce, k);
+                code = path::shadow_code(a.sc, x, a.seed, s.pix[p], s.smp[p], a.mixed ? m.bounce[p] : a.bounce, k);
             }
             ++cast;
         }
@@ -754,53 +846,20 @@ __global__ void k_round_reset(int32_t* counters, int32_t next_mq) {
     counters[C_MQ0 + next_mq] = 0;
 }
 
-// K8: hit shading, BSDF sample, spawn, compaction (render.py:221-244).
 __global__ void k_shade(Args a) {
     const int32_t n = a.ps.counters[a.cur];
     const int32_t* q = pick(a.ps.queue, a.cur);
     int32_t* next = pick(a.ps.queue, a.cur ^ 1);
     int32_t* next_n = &a.ps.counters[a.cur ^ 1];
     const PathState& s = a.ps;
-    const DevScene& sc = a.sc;
     for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
         const int32_t p = q[j];
-        const int32_t f = s.face[p];
-        if (f < 0) continue;
-        const double t = s.t_hit[p];
-        const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
-        const d3 point = {o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
-        const d3 n_raw = mk(sc.normal[3 * f], sc.normal[3 * f + 1], sc.normal[3 * f + 2]);
-        const bool facing = dot(n_raw, d) < 0.0;
-        const d3 nrm = facing ? n_raw : neg(n_raw);
+        if (s.face[p] < 0) continue;
         Acc c;
         load_acc(s, p, c);
-        if (facing) {
-            c.L[0] = c.L[0] + c.Ts[0] * sc.emission[3 * f];
-            c.L[1] = c.L[1] + c.Ts[1] * sc.emission[3 * f + 1];
-            c.L[2] = c.L[2] + c.Ts[2] * sc.emission[3 * f + 2];
-        }
-        const int32_t mi = sc.mesh_of[f];
-        const int32_t kind = sc.mat.kind[mi];
-        const d3 wo = neg(d);
-        const int32_t pix = s.pix[p], smp = s.smp[p];
-        d3 nd;
-        if (kind == 0) {
-            const double u1 = rng::uniform(a.seed, pix, smp, a.bounce, rng::BSDF_U, 0);
-            const double u2 = rng::uniform(a.seed, pix, smp, a.bounce, rng::BSDF_V, 0);
-            nd = path::cosine_sample(nrm, u1, u2);
-        } else if (kind == 1) {
-            nd = path::reflect(wo, nrm);
-        } else {
-            const double u = rng::uniform(a.seed, pix, smp, a.bounce, rng::BSDF_LOBE, 0);
-            nd = path::dielectric_sample(wo, nrm, facing, sc.mat.ior[mi], sc.mat.r0[mi], u);
-        }
-        for (int ch = 0; ch < 3; ++ch) c.Ts[ch] = c.Ts[ch] * sc.mat.rgb[3 * mi + ch];
-        s.ox[p] = point.x + sc.spawn_eps * nd.x;
-        s.oy[p] = point.y + sc.spawn_eps * nd.y;
-        s.oz[p] = point.z + sc.spawn_eps * nd.z;
-        s.dx[p] = nd.x; s.dy[p] = nd.y; s.dz[p] = nd.z;
+        const bool go = shade_one(a, p, a.bounce, c);
         store_acc(s, p, c);
-        if (fmax(fmax(c.Ts[0], c.Ts[1]), c.Ts[2]) >= sc.threshold) next[reserve(next_n)] = p;
+        if (go) next[reserve(next_n)] = p;
     }
 }
 
