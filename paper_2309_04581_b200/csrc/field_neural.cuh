@@ -221,37 +221,40 @@ struct LevelLoads {
     float2 v[8];
 };
 
+// Hashed levels start on a multiple of T entries in the device table
+// (hrt.cu setup_field), so the physical entry off + ((X ^ hY ^ hZ) & mask)
+// equals (X & mask) ^ (hY & mask) ^ ((hZ & mask) | off): per level the six
+// masked terms are formed once, per corner one 3-input XOR (LOP3) gives the
+// texel / element index.
 HRT_DEV void level_issue(const NeuralField& nf, const NeuralLevel& lv, float3 rel, LevelLoads& g,
                          bool tex_level = false) {
     g.c = level_coord(lv, rel);
-    const float2* base = reinterpret_cast<const float2*>(nf.table) + lv.offset;
+    const float2* tab = reinterpret_cast<const float2*>(nf.table);
     const uint32_t X = (uint32_t)g.c.i[0], Y = (uint32_t)g.c.i[1], Z = (uint32_t)g.c.i[2];
+    const uint32_t off = (uint32_t)lv.offset;
     if (lv.dense) {
         const uint32_t r = lv.r, rr = r * r;
-        const uint32_t b0 = X + r * Y + rr * Z;
+        const uint32_t b0 = off + X + r * Y + rr * Z;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            g.v[k] = __ldg(base + (b0 + (uint32_t)(k & 1) + ((k & 2) ? r : 0u) + ((k & 4) ? rr : 0u)));
+            g.v[k] = __ldg(tab + (b0 + (uint32_t)(k & 1) + ((k & 2) ? r : 0u) + ((k & 4) ? rr : 0u)));
     } else {
-        const uint32_t hy0 = Y * kHashY, hy1 = hy0 + kHashY;
-        const uint32_t hz0 = Z * kHashZ, hz1 = hz0 + kHashZ;
+        const uint32_t m = nf.tmask;
+        const uint32_t hy = Y * kHashY, hz = Z * kHashZ;
+        const uint32_t xs[2] = {X & m, (X + 1u) & m};
+        const uint32_t ys[2] = {hy & m, (hy + kHashY) & m};
+        const uint32_t zs[2] = {(hz & m) | off, ((hz + kHashZ) & m) | off};
         if (kFineNoL1 && lv.n >= kFineLevelN) {
             // fine hashed levels have little L1 reuse: keep their fills out of L1
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                g.v[k] = ld_na(base + (((X + (uint32_t)(k & 1)) ^ ((k & 2) ? hy1 : hy0) ^
-                                        ((k & 4) ? hz1 : hz0)) & nf.tmask));
+            for (int k = 0; k < 8; ++k) g.v[k] = ld_na(tab + (xs[k & 1] ^ ys[(k >> 1) & 1] ^ zs[k >> 2]));
         } else if (tex_level) {
-            const uint32_t off = (uint32_t)lv.offset;
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-                g.v[k] = tex1Dfetch<float2>(nf.tex, (int)(off + (((X + (uint32_t)(k & 1)) ^ ((k & 2) ? hy1 : hy0) ^
-                                                                  ((k & 4) ? hz1 : hz0)) & nf.tmask)));
+                g.v[k] = tex1Dfetch<float2>(nf.tex, (int)(xs[k & 1] ^ ys[(k >> 1) & 1] ^ zs[k >> 2]));
         } else {
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                g.v[k] = __ldg(base + (((X + (uint32_t)(k & 1)) ^ ((k & 2) ? hy1 : hy0) ^
-                                        ((k & 4) ? hz1 : hz0)) & nf.tmask));
+            for (int k = 0; k < 8; ++k) g.v[k] = __ldg(tab + (xs[k & 1] ^ ys[(k >> 1) & 1] ^ zs[k >> 2]));
         }
     }
 }

@@ -547,14 +547,22 @@ int setup_field(hrt_handle* h, const hrt_field_desc& fd) {
         nf.tmask = (uint32_t)((1ull << fd.log2_table) - 1);
         for (int a = 0; a < 3; ++a) nf.lo32[a] = (float)fd.bbox_lo[a];
         // Device table: same entries, each level starting on an even entry
-        // (16-byte aligned pairs for the x-pair gathers in encode_level).
+        // (16-byte aligned pairs for the x-pair gathers in encode_level), and
+        // every hashed level on a multiple of T entries, so that its offset
+        // folds into the hash with an OR (nerf::level_issue).
+        const int64_t T = int64_t(1) << fd.log2_table;
         int64_t padded = 0;
         std::vector<int64_t> dev_off(L);
         for (int l = 0; l < L; ++l) {
             const int64_t end = l + 1 < L ? fd.level_offset[l + 1] : fd.n_entries;
+            if (!fd.level_dense[l]) {
+                if (end - fd.level_offset[l] > T) return fail(HRT_EINVAL, "hashed level larger than T");
+                padded = (padded + T - 1) / T * T;
+            }
             dev_off[l] = padded;
             padded += ((end - fd.level_offset[l]) + 1) & ~int64_t(1);
         }
+        if (padded >= (int64_t(1) << 31)) return fail(HRT_EINVAL, "hash table too large");
         std::vector<float> tab((size_t)padded * F, 0.0f);
         for (int l = 0; l < L; ++l) {
             NeuralLevel& lv = nf.lv[l];
