@@ -140,7 +140,7 @@ __device__ __forceinline__ void relu64_tmem(uint32_t accum, uint32_t act) {
         umma::ld16(accum + c0, v);
         uint32_t h[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) h[i] = umma::pack_half2(fmaxf(v[2 * i], 0.f), fmaxf(v[2 * i + 1], 0.f));
+        for (int i = 0; i < 8; ++i) h[i] = umma::pack_half2_relu(v[2 * i], v[2 * i + 1]);
         umma::st<8>(act + c0 / 2, h);
     }
     umma::wait_st();

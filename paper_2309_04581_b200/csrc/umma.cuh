@@ -156,8 +156,17 @@ __device__ __forceinline__ void wait_st() {
 
 // two floats -> packed fp16x2 (round to nearest), low half = first element
 __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
-    __half2 h = __floats2half2_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return r;
+}
+// pack_half2(max(a, 0), max(b, 0)) in one instruction: rounding is monotonic
+// and maps 0 to +0, so ReLU after the fp16 rounding (cvt .relu clamps
+// negatives, -0 included, to +0) gives the same bits as ReLU before it.
+__device__ __forceinline__ uint32_t pack_half2_relu(float a, float b) {
+    uint32_t r;
+    asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return r;
 }
 
 }  // namespace umma
