@@ -453,6 +453,12 @@ template <bool kTrace>
 HRT_DEV bool comp_path(const Args& a, const MarchState& m, int32_t p, int32_t j, int32_t nq,
                        int32_t cnt, double delta, Acc& c, int32_t& done) {
     bool stop = false;
+    // halted() per sample from a running max(T_spec): every channel is
+    // scaled by the same keep >= 0 and rounding is monotonic, so
+    // round(max * keep) is exactly max(round(T_c * keep)) - the same test
+    double tmax = fmax(fmax(c.Ts[0], c.Ts[1]), c.Ts[2]);
+    const double early_t = a.sc.early_t;
+    const int32_t cap = a.sc.sample_cap;
     // rows are read kCompBatch at a time ahead of the (sequential) halt
     // test, so a path waits one memory latency per batch, not per sample
     for (int32_t i0 = 0; i0 < cnt && !stop; i0 += kCompBatch) {
@@ -469,14 +475,15 @@ HRT_DEV bool comp_path(const Args& a, const MarchState& m, int32_t p, int32_t j,
         for (int32_t u = 0; u < kCompBatch; ++u) {
             const int32_t i = i0 + u;
             if (i >= cnt) break;
-            if (halted(a.sc, c)) { stop = true; break; }
+            if ((early_t > 0.0 && tmax < early_t) || (cap > 0 && c.neval >= cap)) { stop = true; break; }
             const float4 f = fb[u];
             const double rgb[3] = {(double)f.y, (double)f.z, (double)f.w};
             const double al = 1.0 - exp(-(double)f.x * delta);
-            const double mask = path::mask_of(a.sc, cb[u]);
+            const double mask = cb[u] == 0 ? 1.0 : path::mask_of(a.sc, cb[u]);
             c.neval += 1;
             ++done;
             composite_m(c, al, rgb, mask);
+            tmax = tmax * (1.0 - al);
             if (kTrace) {
                 const int64_t row = (int64_t)i * nq + j;
                 const int32_t k = m.sk[row];
