@@ -207,6 +207,13 @@ int hrt_refit_rigid(hrt_handle* h, const double* xf, int32_t n_meshes);
 int hrt_set_config(hrt_handle* h, int32_t n_bounces, double threshold, double march_step,
                    double spawn_eps, int32_t sample_cap, double early_t);
 
+/* March schedule of later hrt_render calls (neural field, hybrid mode):
+ * continuous != 0 (default) advances each path to its next bounce inside the
+ * march rounds (all bounces share one wavefront); 0 runs the reference's
+ * bounce-by-bounce loop (render.py:214) - intersect all, march all, shade all.
+ * Both give bit-identical results; this exists for A/B measurement and tests. */
+int hrt_set_march(hrt_handle* h, int32_t continuous);
+
 /* Per-stage device timing of later hrt_render calls into hrt_stats.stage_ms
  * (on != 0) or off (default). Measurement aid: adds one event pair per launch. */
 int hrt_set_profile(hrt_handle* h, int32_t on);

@@ -104,6 +104,7 @@ SIGNATURES = {
                                        ctypes.c_int32, vp, vp]),
     "hrt_set_trace": (ctypes.c_int, [vp, vp, ctypes.c_int64]),
     "hrt_set_profile": (ctypes.c_int, [vp, ctypes.c_int32]),
+    "hrt_set_march": (ctypes.c_int, [vp, ctypes.c_int32]),
     "hrt_set_config": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                       ctypes.c_int32, ctypes.c_double]),
     "hrt_finalize": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, vp, vp, ctypes.c_int64, ctypes.c_int32,

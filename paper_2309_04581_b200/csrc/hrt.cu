@@ -54,6 +54,10 @@ constexpr int64_t kBatchCap = int64_t(1) << HRT_BATCH_CAP_LOG2;   // samples per
 #define HRT_TEX_LEVELS 8
 #endif
 constexpr int kTexLevels = HRT_TEX_LEVELS;        // finest levels gathered via TEX
+#ifndef HRT_MIXED_MARCH
+#define HRT_MIXED_MARCH 1
+#endif
+constexpr bool kMixedMarch = HRT_MIXED_MARCH;     // continuous wavefront march (kern::advance)
 #ifndef HRT_TILED_FRAME
 #define HRT_TILED_FRAME 1
 #endif
@@ -121,6 +125,7 @@ struct hrt_handle {
     int shadow_blocks = 0;
     // hrt_set_profile: event pair per launch, folded into stage_ms
     bool prof = false;
+    bool continuous = kMixedMarch;   // hrt_set_march
     std::vector<cudaEvent_t> pev;
     std::vector<int> pstage;
     int pn = 0;
@@ -842,10 +847,6 @@ constexpr int64_t kMaxRoundSamples = 256;      // (k_round_begin uses the same 2
 #define HRT_ROUNDS_PER_CHECK 2
 #endif
 constexpr int kRoundsPerCheck = HRT_ROUNDS_PER_CHECK;
-#ifndef HRT_MIXED_MARCH
-#define HRT_MIXED_MARCH 1
-#endif
-constexpr bool kMixedMarch = HRT_MIXED_MARCH;     // continuous wavefront march (kern::advance)
 int32_t round_samples(const hrt_handle* h, int64_t live) {
     int64_t S = kern::kRoundSamples;
     if (kTailTiles > 0) {
@@ -1015,7 +1016,7 @@ int run_bounces(hrt_handle* h, kern::Args& a, int64_t paths, int mode, cudaStrea
         if (field && (rc = march(h, a, paths, st))) return rc;
         return HRT_OK;
     }
-    if (kMixedMarch && field && mode == HRT_MODE_HYBRID && !a.trace &&
+    if (h->continuous && field && mode == HRT_MODE_HYBRID && !a.trace &&
         h->sc.field.kind == HRT_FIELD_NEURAL && h->sc.n_bounces >= 1) {
         // continuous wavefront march: bounce 1's rays are intersected here,
         // every later bounce inside the march rounds (kern::advance)
@@ -1148,6 +1149,12 @@ int hrt_set_trace(hrt_handle* h, int32_t* records, int64_t cap) {
     if (!h) return fail(HRT_EINVAL, "null handle");
     h->trace = records;
     h->trace_cap = cap;
+    return HRT_OK;
+}
+
+int hrt_set_march(hrt_handle* h, int32_t continuous) {
+    if (!h) return fail(HRT_EINVAL, "null handle");
+    h->continuous = continuous != 0;
     return HRT_OK;
 }
 

@@ -209,6 +209,10 @@ class Renderer:
         _lib.check(rc, "hrt_intersect")
         return t, f
 
+    def set_march(self, continuous=True):
+        """Continuous wavefront march (default) or the reference's bounce-by-bounce loop."""
+        _lib.check(self.lib.hrt_set_march(self.handle, int(bool(continuous))), "hrt_set_march")
+
     def set_profile(self, on=True):
         """Per-stage device timing of later renders (last_stats['stage_ms'])."""
         _lib.check(self.lib.hrt_set_profile(self.handle, int(bool(on))), "hrt_set_profile")

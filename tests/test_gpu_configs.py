@@ -167,3 +167,33 @@ def test_gpu_rigid_refit_equals_host_moved_scene():
         assert st["nerf_samples"] == ref.last_stats["nerf_samples"]
         ref.close()
     r.close()
+
+
+@pytest.mark.parametrize("which", ["cfg1", "shadows", "cfg2", "moving"])
+def test_gpu_continuous_march_equals_bounce_loop(cuda, which):
+    """The continuous wavefront march (paths advance to their next bounce
+    inside the march rounds, kern::advance) against the reference's
+    bounce-by-bounce loop (render.py:214) on the same renderer: images, NeRF
+    sample counts, shadow rays and bounce rays are identical, bit for bit."""
+    if which == "cfg1":
+        scene, spp, size, cx, cy = configs.cfg1(), 1, 48, 400, 400
+    elif which == "shadows":
+        scene, spp, size, cx, cy = shadow_scene(), 4, 16, 32, 20
+    elif which == "cfg2":
+        scene, spp, size, cx, cy = configs.cfg2(), 4, 16, 256, 300
+    else:
+        scene, spp, size, cx, cy = moving_scene(3), 2, 32, 48, 32
+    r = Renderer(scene)
+    w, h = scene.camera.resolution
+    pix = torch.as_tensor(crop(w, h, size, cx=cx, cy=cy).astype(np.int32), device=cuda)
+    out = {}
+    for continuous in (True, False):
+        r.set_march(continuous)
+        img = r.render_pixels(scene.camera, spp, 5, pixels=pix).cpu().numpy()
+        out[continuous] = (img, dict(r.last_stats))
+    (a, sa), (b, sb) = out[True], out[False]
+    assert np.array_equal(a, b)
+    for key in ("nerf_samples", "shadow_rays", "bounce_rays", "evaluated"):
+        assert sa[key] == sb[key], key
+    assert sa["rounds"] <= sb["rounds"]
+    r.close()
