@@ -272,87 +272,6 @@ HRT_DEV void level_finish(const LevelLoads& g, float* out) {
     out[1] = __fadd_rn(acc[0].y, acc[1].y);
 }
 
-// ---- lane-pair ("x-split") form used by the field engine: the two lanes
-// of a pair encode the same sample, lane dx = 0 the four corners with
-// cx = 0, lane dx = 1 those with cx = 1. x-adjacent corners share a 128-byte
-// line (hashed: 15/16, dense: almost always), so one warp-wide gather touches
-// ~17 lines for 32 corners instead of ~32 lines for 32 corners at the fine
-// levels, halving the L1TEX wavefronts that bound the encode.
-// Definition (oracle/field.py neural_encode): per feature, acc_x =
-// fma-chain over the corners with cx = x in corner order from +0, then
-// feature = acc_0 + acc_1.
-template <int F> struct HalfVec { using T = float2; };
-template <> struct HalfVec<4> { using T = float4; };
-
-template <int F>
-struct HalfLoads {
-    LevelCoord c;
-    typename HalfVec<F>::T v[4];   // corners (cy, cz) = (0,0), (1,0), (0,1), (1,1)
-};
-
-template <int F>
-HRT_DEV void half_issue(const NeuralField& nf, const NeuralLevel& lv, float3 rel, uint32_t dx,
-                        bool valid, HalfLoads<F>& g, bool tex_level = false) {
-    using V = typename HalfVec<F>::T;
-    g.c = level_coord(lv, rel);
-    const V* base = reinterpret_cast<const V*>(nf.table + (size_t)lv.offset * F);
-    const uint32_t X = (uint32_t)g.c.i[0] + dx, Y = (uint32_t)g.c.i[1], Z = (uint32_t)g.c.i[2];
-    uint32_t idx[4];
-    if (lv.dense) {
-        const uint32_t r = lv.r, rr = r * r;
-        const uint32_t b0 = X + r * Y + rr * Z;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) idx[k] = b0 + ((k & 1) ? r : 0u) + ((k & 2) ? rr : 0u);
-    } else {
-        const uint32_t hy0 = Y * kHashY, hy1 = hy0 + kHashY;
-        const uint32_t hz0 = Z * kHashZ, hz1 = hz0 + kHashZ;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) idx[k] = (X ^ ((k & 1) ? hy1 : hy0) ^ ((k & 2) ? hz1 : hz0)) & nf.tmask;
-    }
-    if (tex_level) {
-        const uint32_t off = (uint32_t)lv.offset;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (valid) g.v[k] = tex1Dfetch<V>(nf.tex, (int)(off + idx[k]));
-            else memset(&g.v[k], 0, sizeof(V));
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (valid) g.v[k] = __ldg(base + idx[k]);
-            else memset(&g.v[k], 0, sizeof(V));
-        }
-    }
-}
-
-// Partial sum of this lane's four corners (weights (wx*wy)*wz as in encode_level).
-template <int F>
-HRT_DEV void half_finish(const HalfLoads<F>& g, uint32_t dx, float* out) {
-    const LevelCoord& c = g.c;
-    const float wx = dx ? c.f[0] : __fsub_rn(1.0f, c.f[0]);
-    const float gy = __fsub_rn(1.0f, c.f[1]), gz = __fsub_rn(1.0f, c.f[2]);
-    const float wxy0 = __fmul_rn(wx, gy), wxy1 = __fmul_rn(wx, c.f[1]);
-    float w[4];
-    w[0] = __fmul_rn(wxy0, gz);
-    w[1] = __fmul_rn(wxy1, gz);
-    w[2] = __fmul_rn(wxy0, c.f[2]);
-    w[3] = __fmul_rn(wxy1, c.f[2]);
-    if constexpr (F == 2) {
-        float2 acc = make_float2(0.0f, 0.0f);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) fma2(acc, w[k], g.v[k]);
-        out[0] = acc.x; out[1] = acc.y;
-    } else {
-        float2 a0 = make_float2(0.0f, 0.0f), a1 = make_float2(0.0f, 0.0f);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            fma2(a0, w[k], make_float2(g.v[k].x, g.v[k].y));
-            fma2(a1, w[k], make_float2(g.v[k].z, g.v[k].w));
-        }
-        out[0] = a0.x; out[1] = a0.y; out[2] = a1.x; out[3] = a1.y;
-    }
-}
-
 HRT_DEV float3 rel_coord(const NeuralField& nf, d3 pf) {
     const float3 p = to_f32(pf);
     return make_float3(__fsub_rn(p.x, nf.lo32[0]), __fsub_rn(p.y, nf.lo32[1]),

@@ -49,14 +49,6 @@ __device__ unsigned long long ws_prof[8];
 #ifndef HRT_WS_INFLIGHT
 #define HRT_WS_INFLIGHT 2
 #endif
-#ifndef HRT_LANE_PAIRS
-#define HRT_LANE_PAIRS 0
-#endif
-#ifndef HRT_PAIR_INFLIGHT
-#define HRT_PAIR_INFLIGHT 1
-#endif
-constexpr bool kLanePairs = HRT_LANE_PAIRS;     // x-split corner gathers over lane pairs
-constexpr int kPairInflight = HRT_PAIR_INFLIGHT;   // levels in flight (x2 samples) per lane
 constexpr int kEncWarps = 16;               // 4 level quarters x 4 lane quarters
 constexpr int kInflight = HRT_WS_INFLIGHT;  // levels of gathers in flight per encode thread
 constexpr int kMlpGroups = HRT_WS_GROUPS;
@@ -200,6 +192,9 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
     WS_T0(t_role);
     if (warp < kEncWarps) {
         // ================= encode warps =================
+        // (one code path for all level quarters: warps of all four quarters
+        // share each scheduler, and four specialised copies of this loop
+        // thrash the instruction cache - measured 1.9x slower)
         const int q = warp >> 2;                    // level quarter
         const int r = (warp & 3) * 32 + (threadIdx.x & 31);   // row == TMEM lane
         const float3 lo = make_float3(nf.lo32[0], nf.lo32[1], nf.lo32[2]);
@@ -210,42 +205,6 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
             const int64_t l = t * kRows + r;
             const int64_t i = l < n ? phys_row(rmap, l) : 0;
             float v[NL * F];
-            if constexpr (kLanePairs) {
-                // lane pair (2p, 2p+1) encodes rows 2p and 2p+1 of the quarter;
-                // lane dx gathers the cx = dx corners of both, then the pair
-                // swaps partial sums so lane 2p keeps row 2p, lane 2p+1 row 2p+1
-                const uint32_t dx = threadIdx.x & 1u;
-                const int64_t lA = l - (int64_t)dx;
-                const SampleIn sa = lA < n ? in[phys_row(rmap, lA)] : SampleIn{0.f, 0.f, 0.f, -1};
-                const SampleIn sb = lA + 1 < n ? in[phys_row(rmap, lA + 1)] : SampleIn{0.f, 0.f, 0.f, -1};
-                const bool va = sa.path >= 0, vb = sb.path >= 0;
-                const float3 ra = make_float3(__fsub_rn(sa.x, lo.x), __fsub_rn(sa.y, lo.y),
-                                              __fsub_rn(sa.z, lo.z));
-                const float3 rb = make_float3(__fsub_rn(sb.x, lo.x), __fsub_rn(sb.y, lo.y),
-                                              __fsub_rn(sb.z, lo.z));
-#pragma unroll
-                for (int j = 0; j < NL; j += kPairInflight) {
-                    nerf::HalfLoads<F> ga[kPairInflight], gb[kPairInflight];
-#pragma unroll
-                    for (int u = 0; u < kPairInflight; ++u) {
-                        const bool tx = q * NL + j + u >= nf.tex_from;
-                        nerf::half_issue<F>(nf, nf.lv[q * NL + j + u], ra, dx, va, ga[u], tx);
-                        nerf::half_issue<F>(nf, nf.lv[q * NL + j + u], rb, dx, vb, gb[u], tx);
-                    }
-#pragma unroll
-                    for (int u = 0; u < kPairInflight; ++u) {
-                        float pa[F], pb[F];
-                        nerf::half_finish<F>(ga[u], dx, pa);
-                        nerf::half_finish<F>(gb[u], dx, pb);
-#pragma unroll
-                        for (int f = 0; f < F; ++f) {
-                            const float mine = dx ? pb[f] : pa[f];
-                            const float other = __shfl_xor_sync(0xffffffffu, dx ? pa[f] : pb[f], 1);
-                            v[(j + u) * F + f] = __fadd_rn(dx ? other : mine, dx ? mine : other);
-                        }
-                    }
-                }
-            } else {
             const SampleIn si = l < n ? in[i] : SampleIn{0.f, 0.f, 0.f, -1};
             if (si.path >= 0) {
                 const float3 rel = make_float3(__fsub_rn(si.x, lo.x), __fsub_rn(si.y, lo.y),
@@ -270,7 +229,6 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
             } else {
 #pragma unroll
                 for (int k = 0; k < NL * F; ++k) v[k] = 0.f;
-            }
             }
             uint32_t h[NC];
 #pragma unroll
