@@ -126,6 +126,8 @@ struct hrt_handle {
     // hrt_set_profile: event pair per launch, folded into stage_ms
     bool prof = false;
     bool continuous = kMixedMarch;   // hrt_set_march
+    void* geo_arena = nullptr;       // kern::PathGeo storage (ensure_geo)
+    int64_t geo_n = 0;
     std::vector<cudaEvent_t> pev;
     std::vector<int> pstage;
     int pn = 0;
@@ -150,6 +152,7 @@ struct hrt_handle {
     ~hrt_handle() {
         for (void* p : allocs) cudaFree(p);
         if (arena) cudaFree(arena);
+        if (geo_arena) cudaFree(geo_arena);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         for (cudaEvent_t e : mev) if (e) cudaEventDestroy(e);
@@ -779,6 +782,28 @@ int ensure_state(hrt_handle* h, int64_t paths) {
     return HRT_OK;
 }
 
+// Per-bounce ray geometry of the continuous march (grow only): cap paths x
+// n_bounces x (7 doubles + 1 int).
+int ensure_geo(hrt_handle* h, int32_t n_bounces) {
+    const int64_t need = h->cap * std::max(1, n_bounces);
+    if (need <= h->geo_n) {
+        h->ms.geo.cap = h->cap;
+        return HRT_OK;
+    }
+    if (h->geo_arena) { cudaFree(h->geo_arena); h->geo_arena = nullptr; }
+    const size_t dbl = (size_t)need * 8;
+    CK(cudaMalloc(&h->geo_arena, 7 * dbl + (size_t)need * 4));
+    double* base = static_cast<double*>(h->geo_arena);
+    kern::PathGeo& g = h->ms.geo;
+    g.ox = base; g.oy = base + need; g.oz = base + 2 * need;
+    g.dx = base + 3 * need; g.dy = base + 4 * need; g.dz = base + 5 * need;
+    g.t = base + 6 * need;
+    g.face = reinterpret_cast<int32_t*>(base + 7 * need);
+    g.cap = h->cap;
+    h->geo_n = need;
+    return HRT_OK;
+}
+
 // Persistent host-path buffers (grow only): device pixel list / frame and
 // their pinned host staging copies.
 int ensure_io(hrt_handle* h, int64_t npx) {
@@ -1023,9 +1048,10 @@ int run_bounces(hrt_handle* h, kern::Args& a, int64_t paths, int mode, cudaStrea
         a.bounce = 1;
         a.cur = 0;
         a.mixed = 1;
+        if ((rc = ensure_geo(h, h->sc.n_bounces))) return rc;
         pbeg(h, st);
         kern::k_reset_queue<<<1, 1, 0, st>>>(h->ps.counters, 1);
-        kern::k_intersect<<<g, kThreads, 0, st>>>(a);
+        kern::k_paths<<<g, kThreads, 0, st>>>(a, h->ms.geo);
         CK(cudaGetLastError());
         pend(h, HRT_STAGE_INTERSECT, st);
         h->launches += 2;

@@ -294,6 +294,14 @@ HRT_DEV int32_t dda_next(const NeuralField& nf, const DevField& f, d3 of, d3 df,
 #endif
 constexpr int kRoundSamples = HRT_ROUND_SAMPLES;   // max midpoints per path per round
 
+// Ray geometry of every bounce of a path, traced ahead of the march
+// (continuous march): bounce b (1-based) of path p at [(b - 1) * cap + p].
+struct PathGeo {
+    double *ox, *oy, *oz, *dx, *dy, *dz, *t;    // ray of bounce b (b >= 2) and its nearest-hit t
+    int32_t* face;                              // nearest face of bounce b (-1: miss)
+    int64_t cap;
+};
+
 struct MarchState {         // per path, valid while the path is marching
     double* s0;
     double* delta;
@@ -310,6 +318,7 @@ struct MarchState {         // per path, valid while the path is marching
     struct QRay* shq;       // shadow rays that reach the blocker tree (k_shadow_trace)
     uint64_t* h4;           // per path: rng::prefix(seed, pix, smp, bounce) of this bounce
     int32_t* bounce;        // per path: its current bounce (continuous wavefront march)
+    PathGeo geo;            // per path and bounce: ray + nearest hit (k_paths)
 };
 
 // A queued shadow ray (64 B): origin = the NeRF sample point, float64 as the
@@ -319,29 +328,23 @@ struct __align__(16) QRay {
     int32_t row, idx;
 };
 
-// K8 for one path at its hit of bounce `bounce` (render.py:221-244): normal
-// flip, emission with the post-march throughput, BSDF sample, throughput,
-// spawn. Returns true if the path goes on (hit and max(T_spec) >= threshold).
-HRT_DEV bool shade_one(const Args& a, int32_t p, int32_t bounce, Acc& c) {
-    const PathState& s = a.ps;
+// K8 (render.py:221-244) in two parts. The next ray depends only on the
+// geometry (hit, normal, material) and the keyed RNG, never on the march, so
+// it can be formed ahead of the march (k_paths); the weight update needs the
+// post-march throughput.
+//
+// spawn_ray: normal flip, BSDF sample (RNG keys (pix, smp, bounce)), spawn
+// point + spawn_eps * new direction.
+HRT_DEV void spawn_ray(const Args& a, int32_t pix, int32_t smp, int32_t bounce, d3 o, d3 d, double t,
+                       int32_t f, d3& o2, d3& d2) {
     const DevScene& sc = a.sc;
-    const int32_t f = s.face[p];
-    if (f < 0) return false;
-    const double t = s.t_hit[p];
-    const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
     const d3 point = {o.x + t * d.x, o.y + t * d.y, o.z + t * d.z};
     const d3 n_raw = mk(sc.normal[3 * f], sc.normal[3 * f + 1], sc.normal[3 * f + 2]);
     const bool facing = dot(n_raw, d) < 0.0;
     const d3 nrm = facing ? n_raw : neg(n_raw);
-    if (facing) {
-        c.L[0] = c.L[0] + c.Ts[0] * sc.emission[3 * f];
-        c.L[1] = c.L[1] + c.Ts[1] * sc.emission[3 * f + 1];
-        c.L[2] = c.L[2] + c.Ts[2] * sc.emission[3 * f + 2];
-    }
     const int32_t mi = sc.mesh_of[f];
     const int32_t kind = sc.mat.kind[mi];
     const d3 wo = neg(d);
-    const int32_t pix = s.pix[p], smp = s.smp[p];
     d3 nd;
     if (kind == 0) {
         const double u1 = rng::uniform(a.seed, pix, smp, bounce, rng::BSDF_U, 0);
@@ -353,12 +356,72 @@ HRT_DEV bool shade_one(const Args& a, int32_t p, int32_t bounce, Acc& c) {
         const double u = rng::uniform(a.seed, pix, smp, bounce, rng::BSDF_LOBE, 0);
         nd = path::dielectric_sample(wo, nrm, facing, sc.mat.ior[mi], sc.mat.r0[mi], u);
     }
+    o2 = {point.x + sc.spawn_eps * nd.x, point.y + sc.spawn_eps * nd.y, point.z + sc.spawn_eps * nd.z};
+    d2 = nd;
+}
+
+// shade_weight: emission of a front-facing hit with the post-march T_spec,
+// T_spec *= albedo / reflectance / tint. True if the path goes on
+// (max(T_spec) >= threshold).
+HRT_DEV bool shade_weight(const DevScene& sc, int32_t f, d3 d, Acc& c) {
+    const d3 n_raw = mk(sc.normal[3 * f], sc.normal[3 * f + 1], sc.normal[3 * f + 2]);
+    if (dot(n_raw, d) < 0.0) {
+        c.L[0] = c.L[0] + c.Ts[0] * sc.emission[3 * f];
+        c.L[1] = c.L[1] + c.Ts[1] * sc.emission[3 * f + 1];
+        c.L[2] = c.L[2] + c.Ts[2] * sc.emission[3 * f + 2];
+    }
+    const int32_t mi = sc.mesh_of[f];
     for (int ch = 0; ch < 3; ++ch) c.Ts[ch] = c.Ts[ch] * sc.mat.rgb[3 * mi + ch];
-    s.ox[p] = point.x + sc.spawn_eps * nd.x;
-    s.oy[p] = point.y + sc.spawn_eps * nd.y;
-    s.oz[p] = point.z + sc.spawn_eps * nd.z;
-    s.dx[p] = nd.x; s.dy[p] = nd.y; s.dz[p] = nd.z;
     return fmax(fmax(c.Ts[0], c.Ts[1]), c.Ts[2]) >= sc.threshold;
+}
+
+// Both parts in place (the per-bounce k_shade).
+HRT_DEV bool shade_one(const Args& a, int32_t p, int32_t bounce, Acc& c) {
+    const PathState& s = a.ps;
+    const int32_t f = s.face[p];
+    if (f < 0) return false;
+    const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+    d3 o2, d2;
+    spawn_ray(a, s.pix[p], s.smp[p], bounce, o, d, s.t_hit[p], f, o2, d2);
+    const bool go = shade_weight(a.sc, f, d, c);
+    s.ox[p] = o2.x; s.oy[p] = o2.y; s.oz[p] = o2.z;
+    s.dx[p] = d2.x; s.dy[p] = d2.y; s.dz[p] = d2.z;
+    return go;
+}
+
+// K2 for all bounces of every path: nearest hit of bounce 1, then while the
+// ray hits and bounces remain, the spawned ray of the next bounce and its
+// hit. Same arithmetic as intersect -> shade -> intersect (bit-identical
+// rays); paths later cut by the throughput threshold just leave unused rays.
+__global__ void k_paths(Args a, PathGeo g) {
+    const int32_t n = a.ps.counters[C_Q0];
+    const int32_t* q = a.ps.queue[0];
+    const PathState& s = a.ps;
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const int32_t p = q[j];
+        d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+        const int32_t pix = s.pix[p], smp = s.smp[p];
+        for (int32_t b = 1; b <= a.sc.n_bounces; ++b) {
+            double t = INFINITY;
+            const int32_t f = bvh::nearest(a.sc.bvh, o, d, 0.0, INFINITY, t);
+            const int64_t at = (int64_t)(b - 1) * g.cap + p;
+            g.t[at] = t;
+            g.face[at] = f;
+            if (b == 1) {
+                s.t_hit[p] = t;
+                s.face[p] = f;
+            }
+            if (f < 0 || b == a.sc.n_bounces) break;
+            d3 o2, d2;
+            spawn_ray(a, pix, smp, b, o, d, t, f, o2, d2);
+            o = o2;
+            d = d2;
+            const int64_t nx = at + g.cap;
+            g.ox[nx] = o.x; g.oy[nx] = o.y; g.oz[nx] = o.z;
+            g.dx[nx] = d.x; g.dy[nx] = d.y; g.dz[nx] = d.z;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) stat_add(s.stats, S_SEGMENTS, n);   // bounce-1 rays
 }
 
 // Segment set-up of path p for the march of bounce `bounce`; false (n = 0)
@@ -560,15 +623,18 @@ HRT_DEV bool advance(const Args& a, const MarchState& m, int32_t p, Acc& c, int3
     const PathState& s = a.ps;
     int32_t b = m.bounce[p];
     while (true) {
-        if (!shade_one(a, p, b, c)) return false;
+        const int32_t f = s.face[p];
+        if (f < 0) return false;
+        if (!shade_weight(a.sc, f, mk(s.dx[p], s.dy[p], s.dz[p]), c)) return false;
         if (b >= a.sc.n_bounces) return false;
         ++b;
         m.bounce[p] = b;
-        double t = INFINITY;
-        const int32_t f = bvh::nearest(a.sc.bvh, mk(s.ox[p], s.oy[p], s.oz[p]), mk(s.dx[p], s.dy[p], s.dz[p]),
-                                       0.0, INFINITY, t);
-        s.t_hit[p] = t;
-        s.face[p] = f;
+        // the next bounce's ray and nearest hit, traced ahead by k_paths
+        const int64_t at = (int64_t)(b - 1) * m.geo.cap + p;
+        s.ox[p] = m.geo.ox[at]; s.oy[p] = m.geo.oy[at]; s.oz[p] = m.geo.oz[at];
+        s.dx[p] = m.geo.dx[at]; s.dy[p] = m.geo.dy[at]; s.dz[p] = m.geo.dz[at];
+        s.t_hit[p] = m.geo.t[at];
+        s.face[p] = m.geo.face[at];
         ++segs;
         if (seg_one(a, m, p, b) && !halted(a.sc, c)) return true;
         // nothing to march on this bounce (no segment, or halted): its hit next

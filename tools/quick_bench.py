@@ -1,5 +1,6 @@
 """Quick device timing of one config's frames (development aid; bench.py is
 the contract)."""
+import os
 import sys
 import time
 
@@ -18,6 +19,8 @@ if spp:
     scene.render.spp = spp
 r = Renderer(scene)
 r.set_profile(True)
+if os.environ.get("HRT_MARCH") == "bounce":      # the reference's bounce-by-bounce loop
+    r.set_march(False)
 print(f"cfg{cfg} setup {time.time() - t0:.2f}s", flush=True)
 for it in range(int(sys.argv[4]) if len(sys.argv) > 4 else 4):
     torch.cuda.synchronize()
