@@ -743,7 +743,7 @@ int ensure_state(hrt_handle* h, int64_t paths) {
     if (paths <= h->cap) return HRT_OK;
     if (h->arena) { cudaFree(h->arena); h->arena = nullptr; }
     const int64_t n = paths;
-    const int64_t nb = std::min<int64_t>(n * kern::kRoundSamples, kBatchCap);
+    const int64_t nb = std::min<int64_t>(n * std::max(kern::kRoundSamples, kern::kRoundSamplesSmall), kBatchCap);
     const size_t dbl = (size_t)n * 8, i32 = (size_t)n * 4, f4 = (size_t)n * 16;
     // two passes over the same carve: size it, then assign the pointers
     for (int pass = 0; pass < 2; ++pass) {
@@ -869,7 +869,7 @@ int read_counter(hrt_handle* h, int idx, cudaStream_t st, int32_t* v) {
 constexpr int64_t kTailTiles = HRT_TAIL_TILES;
 constexpr int64_t kMaxRoundSamples = 256;      // (k_round_begin uses the same 256)
 #ifndef HRT_ROUNDS_PER_CHECK
-#define HRT_ROUNDS_PER_CHECK 2
+#define HRT_ROUNDS_PER_CHECK 4
 #endif
 constexpr int kRoundsPerCheck = HRT_ROUNDS_PER_CHECK;
 int32_t round_samples(const hrt_handle* h, int64_t live) {

@@ -293,6 +293,14 @@ HRT_DEV int32_t dda_next(const NeuralField& nf, const DevField& f, d3 of, d3 df,
 #define HRT_ROUND_SAMPLES 32
 #endif
 constexpr int kRoundSamples = HRT_ROUND_SAMPLES;   // max midpoints per path per round
+#ifndef HRT_ROUND_SAMPLES_SMALL
+#define HRT_ROUND_SAMPLES_SMALL 48
+#endif
+#ifndef HRT_SMALL_LIVE
+#define HRT_SMALL_LIVE 200000
+#endif
+constexpr int kRoundSamplesSmall = HRT_ROUND_SAMPLES_SMALL;   // ... when fewer than kSmallLive paths march
+constexpr int kSmallLive = HRT_SMALL_LIVE;
 
 // Ray geometry of every bounce of a path, traced ahead of the march
 // (continuous march): bounce b (1-based) of path p at [(b - 1) * cap + p].
@@ -888,7 +896,9 @@ __global__ void k_round_begin(int32_t* c, unsigned long long* stats, int32_t tar
     c[C_CUR] = cur;
     c[C_FIRST] = c[C_FIRST] == 2 ? 1 : 0;       // 2 = set by k_march_begin
     const int32_t live = c[C_MQ0 + cur];
-    int32_t S = kRoundSamples;
+    // fewer, longer rounds when a GPU's share of paths is small (a round's
+    // k_step floor is a per-path serial chain, so it is paid per round)
+    int32_t S = live >= kSmallLive ? kRoundSamples : kRoundSamplesSmall;
     if (live > 0) {
         S = max(S, min(target_rows / live, 256));
         S = max(1, min(S, batch_cap / live));
