@@ -49,6 +49,10 @@ __device__ unsigned long long ws_prof[8];
 #ifndef HRT_WS_INFLIGHT
 #define HRT_WS_INFLIGHT 2
 #endif
+#ifndef HRT_SYNTH_ENCODE
+#define HRT_SYNTH_ENCODE 0
+#endif
+constexpr bool kSynthEncode = HRT_SYNTH_ENCODE;   // measurement build: MLP fed without gathers
 constexpr int kEncWarps = 16;               // 4 level quarters x 4 lane quarters
 constexpr int kInflight = HRT_WS_INFLIGHT;  // levels of gathers in flight per encode thread
 constexpr int kMlpGroups = HRT_WS_GROUPS;
@@ -209,7 +213,12 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
             if (si.path >= 0) {
                 const float3 rel = make_float3(__fsub_rn(si.x, lo.x), __fsub_rn(si.y, lo.y),
                                                __fsub_rn(si.z, lo.z));
-                if constexpr (F == 2 && NL % kInflight == 0) {
+                if constexpr (kSynthEncode) {
+                    // measurement build only: features from the position, no table
+                    // gathers - what the MLP pipeline sustains when it is fed
+#pragma unroll
+                    for (int k = 0; k < NL * F; ++k) v[k] = 0.01f * (float)k * rel.x - rel.y;
+                } else if constexpr (F == 2 && NL % kInflight == 0) {
                     // kInflight levels of gathers in flight per thread
 #pragma unroll
                     for (int j = 0; j < NL; j += kInflight) {
