@@ -520,7 +520,7 @@ HRT_DEV int32_t gen_path(const Args& a, const MarchState& m, int32_t p, int32_t 
 #endif
 constexpr int32_t kCompBatch = HRT_COMP_BATCH;
 
-template <bool kTrace>
+template <bool kTrace, bool kShadows = true>
 HRT_DEV bool comp_path(const Args& a, const MarchState& m, int32_t p, int32_t j, int32_t nq,
                        int32_t cnt, double delta, Acc& c, int32_t& done) {
     bool stop = false;
@@ -540,7 +540,7 @@ HRT_DEV bool comp_path(const Args& a, const MarchState& m, int32_t p, int32_t j,
             const int64_t row = (int64_t)(i0 + u) * nq + j;
             const bool in = i0 + u < cnt;
             fb[u] = in ? __ldcs(&m.out[row]) : make_float4(0.f, 0.f, 0.f, 0.f);
-            cb[u] = (in && a.sc.em.n > 0) ? __ldcs(&m.shadow[row]) : 0;
+            cb[u] = (kShadows && in && a.sc.em.n > 0) ? __ldcs(&m.shadow[row]) : 0;
         }
 #pragma unroll
         for (int32_t u = 0; u < kCompBatch; ++u) {
@@ -550,7 +550,7 @@ HRT_DEV bool comp_path(const Args& a, const MarchState& m, int32_t p, int32_t j,
             const float4 f = fb[u];
             const double rgb[3] = {(double)f.y, (double)f.z, (double)f.w};
             const double al = 1.0 - exp(-(double)f.x * delta);
-            const double mask = cb[u] == 0 ? 1.0 : path::mask_of(a.sc, cb[u]);
+            const double mask = (!kShadows || cb[u] == 0) ? 1.0 : path::mask_of(a.sc, cb[u]);
             c.neval += 1;
             ++done;
             composite_m(c, al, rgb, mask);
@@ -668,8 +668,10 @@ __global__ void __launch_bounds__(256, HRT_STEP_MINB) k_step(Args a, MarchState 
         load_acc(s, p, c);
         bool go = true;
         if (!first) {
-            const bool stop = comp_path<false>(a, m, p, m.base[p], prev_nq, m.cnt[p], m.delta[p], c,
-                                               done);
+            // (no emitters: the shadow codes are all 0, compile the mask out)
+            const bool stop = a.sc.em.n > 0
+                                  ? comp_path<false, true>(a, m, p, m.base[p], prev_nq, m.cnt[p], m.delta[p], c, done)
+                                  : comp_path<false, false>(a, m, p, m.base[p], prev_nq, m.cnt[p], m.delta[p], c, done);
             go = !stop && !halted(a.sc, c) && m.k[p] < m.n[p];
         } else if (kMixed) {
             go = m.k[p] < m.n[p];
