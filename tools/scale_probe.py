@@ -38,8 +38,12 @@ for world in worlds:
         ms.append(e0.elapsed_time(e1))
         syncs.append(r.last_stats.get("rounds", 0))
     t = sum(ms) / len(ms)
+    r.set_profile(True)
+    r.render_pixels(cams[3], 1, 0, pixels=pix, out=out)
+    stages = " ".join(f"{k}={v:.2f}" for k, v in r.last_stats["stage_ms"].items())
+    r.set_profile(False)
     if base is None:
         base = t * world
     print(f"world {world}: rank-0 share {pix.numel():7d} px  {t:7.3f} ms/frame  "
           f"rounds {sum(syncs) / len(syncs):.0f}  launches {r.last_stats['launches']}  "
-          f"predicted efficiency {base / (world * t):.3f} (vs the first world listed)", flush=True)
+          f"predicted efficiency {base / (world * t):.3f} (vs the first world listed)\n    stages ms: {stages}", flush=True)
