@@ -49,6 +49,9 @@ __device__ unsigned long long ws_prof[8];
 #ifndef HRT_WS_INFLIGHT
 #define HRT_WS_INFLIGHT 2
 #endif
+#ifndef HRT_STREAM_OUT
+#define HRT_STREAM_OUT 1
+#endif
 #ifndef HRT_SYNTH_ENCODE
 #define HRT_SYNTH_ENCODE 0
 #endif
@@ -321,7 +324,11 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
                 rgb[2] = nerf::out_act(o[2], nf.act);
             }
             give();                                         // accumulator free
-            if (path >= 0) out[i] = make_float4(sigma, rgb[0], rgb[1], rgb[2]);
+            if (path >= 0) {
+                const float4 o4 = make_float4(sigma, rgb[0], rgb[1], rgb[2]);
+                if (HRT_STREAM_OUT) __stcs(out + i, o4);      // read once by k_step (evict-first)
+                else out[i] = o4;
+            }
         }
     } else if ((threadIdx.x & 31) == 0) {
         // ================= MMA issuer (one thread) =================

@@ -471,6 +471,16 @@ __global__ void k_seg(Args a, MarchState m) {
 // lanes are neighbouring paths (adjacent pixels) at the same step -> coherent
 // table gathers. Unused rows of the path become holes (path = -1) that the
 // field engine skips. Returns the count.
+// Batch rows are written once and read by the next kernel: streaming
+// stores (evict-first), so they do not push the hash table out of L2.
+#ifndef HRT_STREAM_ROWS
+#define HRT_STREAM_ROWS 1
+#endif
+HRT_DEV void st_row(fws::SampleIn* p, const fws::SampleIn& r) {
+    if (HRT_STREAM_ROWS) __stcs(reinterpret_cast<float4*>(p), *reinterpret_cast<const float4*>(&r));
+    else *p = r;
+}
+
 HRT_DEV int32_t gen_path(const Args& a, const MarchState& m, int32_t p, int32_t j, int32_t nq,
                          int32_t S, const Acc& c) {
     const PathState& s = a.ps;
@@ -492,7 +502,7 @@ HRT_DEV int32_t gen_path(const Args& a, const MarchState& m, int32_t p, int32_t 
                 const float3 p32 = nerf::to_f32(xf);
                 fws::SampleIn r;
                 r.x = p32.x; r.y = p32.y; r.z = p32.z; r.path = p;
-                m.in[(int64_t)cnt * nq + j] = r;
+                st_row(&m.in[(int64_t)cnt * nq + j], r);
                 if (a.sc.em.n > 0 || a.trace) m.sk[(int64_t)cnt * nq + j] = k;   // read by shadows / trace only
                 ++cnt;
                 ++k;
@@ -505,7 +515,7 @@ HRT_DEV int32_t gen_path(const Args& a, const MarchState& m, int32_t p, int32_t 
         fws::SampleIn r;
         r.x = r.y = r.z = 0.f;
         r.path = -1;
-        m.in[(int64_t)i * nq + j] = r;
+        st_row(&m.in[(int64_t)i * nq + j], r);
     }
     m.cnt[p] = cnt;
     m.k[p] = k;

@@ -193,7 +193,43 @@ def test_gpu_continuous_march_equals_bounce_loop(cuda, which):
         out[continuous] = (img, dict(r.last_stats))
     (a, sa), (b, sb) = out[True], out[False]
     assert np.array_equal(a, b)
-    for key in ("nerf_samples", "shadow_rays", "bounce_rays", "evaluated"):
+    # ("evaluated" counts field-engine rows incl. samples generated past an
+    # early-out inside a batch; it depends on the round sizes, not a result)
+    for key in ("nerf_samples", "shadow_rays", "bounce_rays"):
         assert sa[key] == sb[key], key
     assert sa["rounds"] <= sb["rounds"]
+    r.close()
+
+
+@pytest.mark.parametrize("n_bounces,threshold,sample_cap,early_t", [
+    (0, 1e-4, 1024, 1e-4),       # march only, no surface interaction
+    (1, 1e-4, 1024, 1e-4),
+    (6, 1e-4, 1024, 1e-4),       # more bounces than most paths live
+    (4, 0.5, 1024, 1e-4),        # throughput threshold kills paths at their first hit
+    (4, 1e-4, 1, 1e-4),          # sample cap reached on the first sample: later bounces march nothing
+    (4, 1e-4, 37, 1e-4),         # cap in the middle of a round / bounce
+    (4, 1e-4, 0, 0.6),           # early-out after a few samples, then shading continues
+])
+def test_gpu_continuous_march_edge_configs(cuda, n_bounces, threshold, sample_cap, early_t):
+    """Continuous march vs the bounce-by-bounce loop on RenderConfig edges
+    (hrt_set_config): halted paths (cap / early-out) must still be shaded and
+    continue through their remaining bounces with zero samples, exactly as
+    the per-bounce loop does."""
+    scene = moving_scene(5)
+    r = Renderer(scene)
+    cfg = (n_bounces, threshold, scene.render.march_step, r.pack["spawn_eps"], sample_cap, early_t)
+    r.set_config(cfg)
+    w, h = scene.camera.resolution
+    pix = torch.as_tensor(crop(w, h, 32, cx=48, cy=32).astype(np.int32), device=cuda)
+    out = {}
+    for continuous in (True, False):
+        r.set_march(continuous)
+        img = r.render_pixels(scene.camera, 2, 9, pixels=pix).cpu().numpy()
+        out[continuous] = (img, dict(r.last_stats))
+    (a, sa), (b, sb) = out[True], out[False]
+    assert np.array_equal(a, b)
+    for key in ("nerf_samples", "bounce_rays"):
+        assert sa[key] == sb[key], key
+    if sample_cap == 1:
+        assert sa["nerf_samples"] <= 2 * pix.numel()
     r.close()
