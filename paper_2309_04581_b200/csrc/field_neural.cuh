@@ -216,20 +216,27 @@ HRT_DEV float2 ld_na(const float2* p) {
     return v;
 }
 
-struct LevelLoads {
+template <int F> struct FVec { using T = float2; };
+template <> struct FVec<4> { using T = float4; };
+
+template <int F>
+struct LevelLoadsF {
     LevelCoord c;
-    float2 v[8];
+    typename FVec<F>::T v[8];
 };
+using LevelLoads = LevelLoadsF<2>;
 
 // Hashed levels start on a multiple of T entries in the device table
 // (hrt.cu setup_field), so the physical entry off + ((X ^ hY ^ hZ) & mask)
 // equals (X & mask) ^ (hY & mask) ^ ((hZ & mask) | off): per level the six
 // masked terms are formed once, per corner one 3-input XOR (LOP3) gives the
 // texel / element index.
-HRT_DEV void level_issue(const NeuralField& nf, const NeuralLevel& lv, float3 rel, LevelLoads& g,
+template <int F = 2>
+HRT_DEV void level_issue(const NeuralField& nf, const NeuralLevel& lv, float3 rel, LevelLoadsF<F>& g,
                          bool tex_level = false) {
+    using V = typename FVec<F>::T;
     g.c = level_coord(lv, rel);
-    const float2* tab = reinterpret_cast<const float2*>(nf.table);
+    const V* tab = reinterpret_cast<const V*>(nf.table);
     const uint32_t X = (uint32_t)g.c.i[0], Y = (uint32_t)g.c.i[1], Z = (uint32_t)g.c.i[2];
     const uint32_t off = (uint32_t)lv.offset;
     if (lv.dense) {
@@ -244,14 +251,18 @@ HRT_DEV void level_issue(const NeuralField& nf, const NeuralLevel& lv, float3 re
         const uint32_t xs[2] = {X & m, (X + 1u) & m};
         const uint32_t ys[2] = {hy & m, (hy + kHashY) & m};
         const uint32_t zs[2] = {(hz & m) | off, ((hz + kHashZ) & m) | off};
-        if (kFineNoL1 && lv.n >= kFineLevelN) {
+        if (F == 2 && kFineNoL1 && lv.n >= kFineLevelN) {
             // fine hashed levels have little L1 reuse: keep their fills out of L1
 #pragma unroll
-            for (int k = 0; k < 8; ++k) g.v[k] = ld_na(tab + (xs[k & 1] ^ ys[(k >> 1) & 1] ^ zs[k >> 2]));
+            for (int k = 0; k < 8; ++k) {
+                const float2 t = ld_na(reinterpret_cast<const float2*>(nf.table) +
+                                       (xs[k & 1] ^ ys[(k >> 1) & 1] ^ zs[k >> 2]));
+                g.v[k] = *reinterpret_cast<const V*>(&t);
+            }
         } else if (tex_level) {
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-                g.v[k] = tex1Dfetch<float2>(nf.tex, (int)(xs[k & 1] ^ ys[(k >> 1) & 1] ^ zs[k >> 2]));
+                g.v[k] = tex1Dfetch<V>(nf.tex, (int)(xs[k & 1] ^ ys[(k >> 1) & 1] ^ zs[k >> 2]));
         } else {
 #pragma unroll
             for (int k = 0; k < 8; ++k) g.v[k] = __ldg(tab + (xs[k & 1] ^ ys[(k >> 1) & 1] ^ zs[k >> 2]));
@@ -259,17 +270,32 @@ HRT_DEV void level_issue(const NeuralField& nf, const NeuralLevel& lv, float3 re
     }
 }
 
-HRT_DEV void level_finish(const LevelLoads& g, float* out) {
+template <int F = 2>
+HRT_DEV void level_finish(const LevelLoadsF<F>& g, float* out) {
     const LevelCoord& c = g.c;
     const float gx = __fsub_rn(1.0f, c.f[0]), gy = __fsub_rn(1.0f, c.f[1]),
                 gz = __fsub_rn(1.0f, c.f[2]);
     const float wxy[4] = {__fmul_rn(gx, gy), __fmul_rn(c.f[0], gy), __fmul_rn(gx, c.f[1]),
                           __fmul_rn(c.f[0], c.f[1])};
-    float2 acc[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
+    if constexpr (F == 2) {
+        float2 acc[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
 #pragma unroll
-    for (int k = 0; k < 8; ++k) fma2(acc[k & 1], __fmul_rn(wxy[k & 3], (k & 4) ? c.f[2] : gz), g.v[k]);
-    out[0] = __fadd_rn(acc[0].x, acc[1].x);
-    out[1] = __fadd_rn(acc[0].y, acc[1].y);
+        for (int k = 0; k < 8; ++k) fma2(acc[k & 1], __fmul_rn(wxy[k & 3], (k & 4) ? c.f[2] : gz), g.v[k]);
+        out[0] = __fadd_rn(acc[0].x, acc[1].x);
+        out[1] = __fadd_rn(acc[0].y, acc[1].y);
+    } else {
+        // same chains as gather_accumulate<4>: features (0,1) and (2,3) as FFMA2 pairs
+        float2 a0[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
+        float2 a1[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float w = __fmul_rn(wxy[k & 3], (k & 4) ? c.f[2] : gz);
+            fma2(a0[k & 1], w, make_float2(g.v[k].x, g.v[k].y));
+            fma2(a1[k & 1], w, make_float2(g.v[k].z, g.v[k].w));
+        }
+        out[0] = __fadd_rn(a0[0].x, a0[1].x); out[1] = __fadd_rn(a0[0].y, a0[1].y);
+        out[2] = __fadd_rn(a1[0].x, a1[1].x); out[3] = __fadd_rn(a1[0].y, a1[1].y);
+    }
 }
 
 HRT_DEV float3 rel_coord(const NeuralField& nf, d3 pf) {

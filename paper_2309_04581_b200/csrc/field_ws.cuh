@@ -58,6 +58,11 @@ __device__ unsigned long long ws_prof[8];
 constexpr bool kSynthEncode = HRT_SYNTH_ENCODE;   // measurement build: MLP fed without gathers
 constexpr int kEncWarps = 16;               // 4 level quarters x 4 lane quarters
 constexpr int kInflight = HRT_WS_INFLIGHT;  // levels of gathers in flight per encode thread
+#ifndef HRT_WS_INFLIGHT4
+#define HRT_WS_INFLIGHT4 1
+#endif
+template <int F>
+constexpr int kInflightF = F == 2 ? kInflight : HRT_WS_INFLIGHT4;   // F = 4: 16-B gathers
 constexpr int kMlpGroups = HRT_WS_GROUPS;
 constexpr int kMlpWarps = 4 * kMlpGroups;
 constexpr int kThreads = 32 * (kEncWarps + kMlpWarps + 1);   // + MMA issuer warp
@@ -221,17 +226,18 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
                     // gathers - what the MLP pipeline sustains when it is fed
 #pragma unroll
                     for (int k = 0; k < NL * F; ++k) v[k] = 0.01f * (float)k * rel.x - rel.y;
-                } else if constexpr (F == 2 && NL % kInflight == 0) {
-                    // kInflight levels of gathers in flight per thread
+                } else if constexpr (NL % kInflightF<F> == 0) {
+                    // kInflightF levels of gathers in flight per thread
+                    constexpr int IF = kInflightF<F>;
 #pragma unroll
-                    for (int j = 0; j < NL; j += kInflight) {
-                        nerf::LevelLoads g[kInflight];
+                    for (int j = 0; j < NL; j += IF) {
+                        nerf::LevelLoadsF<F> g[IF];
 #pragma unroll
-                        for (int u = 0; u < kInflight; ++u)
-                            nerf::level_issue(nf, nf.lv[q * NL + j + u], rel, g[u],
-                                              q * NL + j + u >= nf.tex_from);
+                        for (int u = 0; u < IF; ++u)
+                            nerf::level_issue<F>(nf, nf.lv[q * NL + j + u], rel, g[u],
+                                                 q * NL + j + u >= nf.tex_from);
 #pragma unroll
-                        for (int u = 0; u < kInflight; ++u) nerf::level_finish(g[u], v + (j + u) * F);
+                        for (int u = 0; u < IF; ++u) nerf::level_finish<F>(g[u], v + (j + u) * F);
                     }
                 } else {
 #pragma unroll
