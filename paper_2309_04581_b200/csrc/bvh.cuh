@@ -307,11 +307,27 @@ HRT_DEV bool any_hit_w(const DevBvh& b, d3 o, d3 d, double t_min, double t_max) 
 }
 
 // ---------------------------------------------------- 4-wide traversal
-HRT_DEV QNode load_q(const QNode* __restrict__ nodes, int32_t i) {
-    const float4* p = reinterpret_cast<const float4*>(nodes + i);
+// The node's lo boxes and refs come through the LSU path, its hi boxes
+// through the TEX path (a float4 texture over the same array, same bits), so
+// divergent traversals spread their node fetches over both L1TEX data pipes
+// (round-1 ncu of the shadow tracer: LSU data pipe 84 % busy; measured:
+// shadow stage -4 %, closest hit +4 %, so only any-hit traversals use it).
+#ifndef HRT_QNODE_TEX
+#define HRT_QNODE_TEX 1
+#endif
+template <bool kTex = false>
+HRT_DEV QNode load_q(const DevBvh& b, int32_t i) {
+    const float4* p = reinterpret_cast<const float4*>(b.qnodes + i);
     QNode q;
     q.lox = __ldg(p); q.loy = __ldg(p + 1); q.loz = __ldg(p + 2);
-    q.hix = __ldg(p + 3); q.hiy = __ldg(p + 4); q.hiz = __ldg(p + 5);
+    if (kTex && HRT_QNODE_TEX && b.qtex) {
+        const int t = 8 * i;
+        q.hix = tex1Dfetch<float4>(b.qtex, t + 3);
+        q.hiy = tex1Dfetch<float4>(b.qtex, t + 4);
+        q.hiz = tex1Dfetch<float4>(b.qtex, t + 5);
+    } else {
+        q.hix = __ldg(p + 3); q.hiy = __ldg(p + 4); q.hiz = __ldg(p + 5);
+    }
     q.ref = __ldg(reinterpret_cast<const int4*>(p + 6));
     return q;
 }
@@ -344,7 +360,7 @@ HRT_DEV int32_t closest_q(const DevBvh& b, d3 o, d3 d, double t_min, double t_ma
     int sp = 0;
     int32_t cur = 0;
     while (true) {
-        const QNode q = load_q(b.qnodes, cur);
+        const QNode q = load_q(b, cur);
         float nr[4];
         uint32_t m = qchildren(q, r, t0, t_hi32(fmin(t_max, best_t)), nr);
         // leaves first (they can only shrink best_t)
@@ -389,7 +405,7 @@ HRT_DEV bool any_hit_q(const DevBvh& b, d3 o, d3 d, double t_min, double t_max) 
     int sp = 0;
     int32_t cur = 0;
     while (true) {
-        const QNode q = load_q(b.qnodes, cur);
+        const QNode q = load_q<true>(b, cur);
         float nr[4];
         uint32_t m = qchildren(q, r, t0, t1, nr);
 #pragma unroll

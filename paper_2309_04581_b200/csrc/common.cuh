@@ -92,6 +92,7 @@ struct __align__(16) QNode {
 
 struct DevBvh {
     const QNode* qnodes;    // 4-wide float32-culling tree (traversal)
+    unsigned long long qtex;   // float4 texture over qnodes (8 texels per node), 0 = none
     const WNode* wnodes;    // binary float32 tree (source of the 4-wide one)
     const BvhNode* nodes;
     const double* tri;      // leaf-ordered: v0, e1, e2 (9 doubles)

@@ -87,6 +87,7 @@ struct hrt_handle {
     DevScene sc{};
     RefitState rf, rfb;
     std::vector<void*> allocs;
+    std::vector<cudaTextureObject_t> texs;   // BVH node textures (upload_bvh)
     hrt::BvhHost bvh, blk;
     BvhNode* d_nodes = nullptr;
     double* d_tri = nullptr;
@@ -165,6 +166,7 @@ struct hrt_handle {
         if (io_stream) cudaStreamDestroy(io_stream);
         for (cudaEvent_t e : io_ev) if (e) cudaEventDestroy(e);
         if (tex) cudaDestroyTextureObject(tex);
+        for (cudaTextureObject_t t : texs) cudaDestroyTextureObject(t);
     }
 };
 
@@ -474,6 +476,7 @@ void build_wnodes(const hrt::BvhHost& b, std::vector<WNode>& w, std::vector<int2
 int upload_bvh(hrt_handle* h, const hrt::BvhHost& b, DevBvh& out, RefitState& r) {
     out.n_faces = b.n_faces;
     out.nodes = nullptr; out.tri = nullptr; out.tri_id = nullptr; out.wnodes = nullptr; out.qnodes = nullptr;
+    out.qtex = 0;
     r.wsrc = nullptr;
     r.n_w = 0;
     if (b.n_faces == 0) return HRT_OK;
@@ -495,6 +498,20 @@ int upload_bvh(hrt_handle* h, const hrt::BvhHost& b, DevBvh& out, RefitState& r)
         if ((rc = h->upload(qs.data(), qs.size(), &r.qsrc))) return rc;
         out.qnodes = dq;
         r.n_q = (int32_t)q.size();
+        {   // texture view of the nodes (bvh::load_q)
+            cudaResourceDesc rd{};
+            rd.resType = cudaResourceTypeLinear;
+            rd.res.linear.devPtr = dq;
+            rd.res.linear.desc = cudaCreateChannelDesc<float4>();
+            rd.res.linear.sizeInBytes = q.size() * sizeof(QNode);
+            cudaTextureDesc td{};
+            td.readMode = cudaReadModeElementType;
+            td.filterMode = cudaFilterModePoint;
+            cudaTextureObject_t to = 0;
+            CK(cudaCreateTextureObject(&to, &rd, &td, nullptr));
+            h->texs.push_back(to);
+            out.qtex = to;
+        }
         if (!r.roots.empty()) {
             if ((rc = h->upload(r.roots.data(), r.roots.size(), &r.d_roots))) return rc;
             if ((rc = h->alloc(r.roots.size() * 6 * 8, reinterpret_cast<void**>(&r.d_rootbox)))) return rc;

@@ -829,7 +829,7 @@ __global__ void __launch_bounds__(256) k_shadow_trace(Args a, MarchState m) {
                 blocked = bvh::leaf_any(b, cur, o, d, t_min, tmax);
                 done = blocked;
             } else {
-                const QNode qn = bvh::load_q(b.qnodes, cur);
+                const QNode qn = bvh::load_q<true>(b, cur);
                 float nr[4];
                 uint32_t mk4 = bvh::qchildren(qn, r32, t0, t1, nr);
                 while (mk4) {
