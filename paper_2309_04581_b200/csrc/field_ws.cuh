@@ -44,7 +44,7 @@ __device__ unsigned long long ws_prof[8];
 #define HRT_WS_GROUPS 2
 #endif
 #ifndef HRT_WS_STAGES
-#define HRT_WS_STAGES 4
+#define HRT_WS_STAGES 6
 #endif
 #ifndef HRT_WS_INFLIGHT
 #define HRT_WS_INFLIGHT 2
@@ -66,7 +66,12 @@ constexpr int kInflightF = F == 2 ? kInflight : HRT_WS_INFLIGHT4;   // F = 4: 16
 constexpr int kMlpGroups = HRT_WS_GROUPS;
 constexpr int kMlpWarps = 4 * kMlpGroups;
 constexpr int kThreads = 32 * (kEncWarps + kMlpWarps + 1);   // + MMA issuer warp
-constexpr int kStages = HRT_WS_STAGES;
+constexpr int kMaxStages = 8;                 // barrier slots reserved per ring
+// encoded-tile ring depth: HRT_WS_STAGES tiles of E/2 TMEM columns, within the
+// 128 columns below the MLP groups' (measured on cfg1: 6 stages 1 % faster than 4)
+template <int E>
+constexpr int kStagesE = HRT_WS_STAGES * (E / 2) <= 128 ? HRT_WS_STAGES : 128 / (E / 2);
+static_assert(HRT_WS_STAGES <= kMaxStages, "stage ring");
 constexpr int kRows = 128;
 constexpr uint32_t kTmemCols = 512;
 
@@ -113,14 +118,14 @@ __host__ __device__ constexpr SmemPlan plan(int E) {
     return {0u, nerf::woff(E).total, nerf::woff(E).total + 256u, nerf::woff(E).total + 272u};
 }
 
-// barrier slots (8 B each): full[kStages] (encoders -> MMA), empty[kStages]
+// barrier slots (8 B each): full[kMaxStages] (encoders -> MMA), empty[kMaxStages]
 // (MMA commit -> encoders), accf[g] (MMA commit -> epilogue g), actr[g]
 // (epilogue g -> MMA: activations written / accumulator consumed)
 __device__ __forceinline__ uint32_t bar_full(uint32_t base, int s) { return base + 8u * s; }
-__device__ __forceinline__ uint32_t bar_empty(uint32_t base, int s) { return base + 8u * (kStages + s); }
-__device__ __forceinline__ uint32_t bar_accf(uint32_t base, int g) { return base + 8u * (2 * kStages + g); }
+__device__ __forceinline__ uint32_t bar_empty(uint32_t base, int s) { return base + 8u * (kMaxStages + s); }
+__device__ __forceinline__ uint32_t bar_accf(uint32_t base, int g) { return base + 8u * (2 * kMaxStages + g); }
 __device__ __forceinline__ uint32_t bar_actr(uint32_t base, int g) {
-    return base + 8u * (2 * kStages + kMlpGroups + g);
+    return base + 8u * (2 * kMaxStages + kMlpGroups + g);
 }
 
 __device__ __forceinline__ void arrive(uint32_t bar) {
@@ -165,6 +170,7 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
     constexpr int NL = L / 4;                     // levels per encode thread
     constexpr int NC = NL * F / 2;                // TMEM columns per encode thread
     constexpr uint32_t kStageCols = E / 2;
+    constexpr int kStages = kStagesE<E>;
     const int warp = threadIdx.x >> 5;
     if (round_ctr) {                 // device-driven march round (kern::k_round_begin counters)
         set_rows(rmap, round_ctr[C_MQ0 + (round_ctr[C_CUR] ^ 1)], round_ctr[C_STRIDE]);
