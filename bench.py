@@ -123,9 +123,10 @@ def peaks():
 
 
 def ncu_traffic():
-    """Per-launch DRAM bytes and L2->L1 sectors per sample of the field engine
-    from the committed ncu capture (profiles/r01_field_traffic.json)."""
-    path = os.path.join(ROOT, "profiles", "r01_field_traffic.json")
+    """Per-launch DRAM bytes and L2->L1 requests / sectors per sample of the
+    field engine from the committed ncu capture (profiles/r01e_field_traffic.json,
+    made by tools/field_traffic.py)."""
+    path = os.path.join(ROOT, "profiles", "r01e_field_traffic.json")
     try:
         with open(path) as f:
             return json.load(f)
@@ -388,7 +389,8 @@ def run_ours(args, rank, world, local):
         traffic = ncu_traffic() or {}
         field_sps = march_samples / (march_ms * 1e-3)                      # samples/s inside the engine
         sec_per_sample = traffic.get("l2_sectors_per_sample")
-        peak_sectors = gather_gbs * 1e9 / 8.0                              # one sector per random gather
+        req_per_sample = traffic.get("l2_requests_per_sample")
+        peak_requests = gather_gbs * 1e9 / 8.0                             # one request per random 8-B gather
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
@@ -415,14 +417,15 @@ def run_ours(args, rank, world, local):
                                "so frac > 1 vs HBM: the real limiter is roofline_gather",
             },
             "roofline_gather": {
-                "bound": "l2->l1 random-sector gathers (L1 miss path, ~1 sector/clk/SM)",
-                "achieved": field_sps * sec_per_sample if sec_per_sample else None,
-                "peak": peak_sectors, "unit": "sectors/s",
-                "frac": field_sps * sec_per_sample / peak_sectors if sec_per_sample else None,
-                "sectors_per_sample": sec_per_sample,
+                "bound": "L1 miss requests to L2 (random gathers, ~1 request/clk/SM)",
+                "achieved": field_sps * req_per_sample if req_per_sample else None,
+                "peak": peak_requests, "unit": "requests/s",
+                "frac": field_sps * req_per_sample / peak_requests if req_per_sample else None,
+                "requests_per_sample": req_per_sample, "sectors_per_sample": sec_per_sample,
                 "peak_source": "hrt_gather_peak (live, this run): independent random 8-B gathers over the "
-                               f"same table, {gather_gbs:.0f} GB/s useful; sectors/sample from "
-                               "profiles/r01_field_traffic.json (ncu lts__t_sectors_srcunit_tex_op_read)",
+                               f"same table, {gather_gbs:.0f} GB/s useful = 1 request each; requests/sample from "
+                               "profiles/r01e_field_traffic.json (ncu lts__t_requests_srcunit_tex_op_read over a "
+                               "frame's field-engine launches)",
             },
             "roofline_mlp": {"bound": "tensor", "achieved": march_samples * mlp_flop / (march_ms * 1e-3) / 1e12,
                              "peak": tflops, "unit": "TFLOP/s",
