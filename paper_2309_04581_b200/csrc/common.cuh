@@ -204,6 +204,8 @@ enum Counter { C_Q0 = 0, C_Q1 = 1, C_FETCH = 2,
                C_CUR = 12, C_FIRST = 13, C_S = 14, C_STRIDE = 15, C_PSTRIDE = 16,
                // shadow-ray queue of a round: length, fetch cursor of the tracer
                C_SHQ = 17, C_SHF = 18,
+               // k_step in tail mode (G lanes per path) this round
+               C_TAIL = 19,
                C_COUNT = 16 };
 
 HRT_DEV d3 field_point(const DevField& f, d3 p) {

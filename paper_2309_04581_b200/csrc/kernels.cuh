@@ -659,6 +659,188 @@ HRT_DEV bool advance(const Args& a, const MarchState& m, int32_t p, Acc& c, int3
     }
 }
 
+// ---- tail rounds: G lanes per path (continuous march, few marching paths).
+// A round's k_step is a per-path serial chain; when few paths remain (the
+// last rounds, or a GPU's small share) the SMs idle and that chain is the
+// round's floor. Here G lanes split its independent parts - lane i loads
+// sample i0 + i and forms its opacity (the fp64 exp), tests candidate k + i
+// (position, box, occupancy) - and lane 0 alone runs the compositing
+// recurrence and the advance, in the same order with the same operations as
+// comp_path / gen_path / advance, so results are bit-identical.
+#ifndef HRT_TAIL_LANES
+#define HRT_TAIL_LANES 8
+#endif
+#ifndef HRT_TAIL_LIVE
+#define HRT_TAIL_LIVE 16384
+#endif
+constexpr int kTailLanes = HRT_TAIL_LANES;
+constexpr int kTailLive = HRT_TAIL_LIVE;      // k_round_begin: tail mode below this many paths
+
+template <int G>
+struct Grp {
+    uint32_t gl, gbase, gmask;
+    HRT_DEV Grp() {
+        const uint32_t lane = threadIdx.x & 31u;
+        gl = lane % G;
+        gbase = lane - gl;
+        gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
+    }
+    template <class T>
+    HRT_DEV T bcast(T v, uint32_t src) const { return __shfl_sync(gmask, v, (int)(gbase + src)); }
+    HRT_DEV uint32_t ballot(bool v) const { return (__ballot_sync(gmask, v) & gmask) >> gbase; }
+};
+
+template <int G, bool kShadows>
+HRT_DEV bool comp_path_tail(const Args& a, const MarchState& m, int32_t j, int32_t nq, int32_t cnt,
+                            double delta, Acc& c, int32_t& done, const Grp<G>& g) {
+    bool stop = false;
+    double tmax = fmax(fmax(c.Ts[0], c.Ts[1]), c.Ts[2]);
+    const double early_t = a.sc.early_t;
+    const int32_t cap = a.sc.sample_cap;
+    for (int32_t i0 = 0; i0 < cnt && !stop; i0 += G) {
+        const int32_t i = i0 + (int32_t)g.gl;
+        const int64_t row = (int64_t)i * nq + j;
+        const bool in = i < cnt;
+        const float4 f = in ? __ldcs(&m.out[row]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int32_t cb = (kShadows && in && a.sc.em.n > 0) ? __ldcs(&m.shadow[row]) : 0;
+        const double al = 1.0 - exp(-(double)f.x * delta);
+        const double mask = (!kShadows || cb == 0) ? 1.0 : path::mask_of(a.sc, cb);
+        const int32_t nu = min(G, cnt - i0);
+        for (int32_t u = 0; u < nu; ++u) {
+            const double alu = g.bcast(al, (uint32_t)u), mu = g.bcast(mask, (uint32_t)u);
+            const double rgb[3] = {(double)g.bcast(f.y, (uint32_t)u), (double)g.bcast(f.z, (uint32_t)u),
+                                   (double)g.bcast(f.w, (uint32_t)u)};
+            if (g.gl == 0 && !stop) {
+                if ((early_t > 0.0 && tmax < early_t) || (cap > 0 && c.neval >= cap)) {
+                    stop = true;
+                } else {
+                    c.neval += 1;
+                    ++done;
+                    composite_m(c, alu, rgb, mu);
+                    tmax = tmax * (1.0 - alu);
+                }
+            }
+        }
+        stop = g.bcast((int32_t)stop, 0) != 0;
+    }
+    return stop;
+}
+
+template <int G>
+HRT_DEV int32_t gen_path_tail(const Args& a, const MarchState& m, int32_t p, int32_t j, int32_t nq,
+                              int32_t S, int32_t neval, bool halt, const Grp<G>& g) {
+    const PathState& s = a.ps;
+    const DevField& fld = a.sc.field;
+    const NeuralField& nf = fld.nf;
+    int32_t budget = S;
+    if (a.sc.sample_cap > 0) budget = min(budget, a.sc.sample_cap - neval);
+    int32_t cnt = 0, k = m.k[p];
+    const bool write_k = a.sc.em.n > 0;
+    if (!halt) {
+        const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+        const Segment sg{m.s0[p], m.delta[p], m.n[p]};
+        const d3 of = field_point(fld, o), df = field_dir(fld, d);
+        while (cnt < budget && k < sg.n) {
+            const int32_t kk = k + (int32_t)g.gl;
+            const d3 xf = field_point(fld, sample_point(o, d, sg, kk));
+            const bool ins = kk < sg.n && inside_box(fld.lo, fld.hi, xf);
+            int32_t cell3[3] = {0, 0, 0};
+            bool ev = false;
+            if (ins) ev = nerf::occ_test(nf, nerf::occ_cell(nf, xf, cell3));
+            const uint32_t bal = g.ballot(ev);
+            const int32_t rank = __popc(bal & ((1u << g.gl) - 1u));
+            if (ev && cnt + rank < budget) {
+                const float3 p32 = nerf::to_f32(xf);
+                fws::SampleIn r;
+                r.x = p32.x; r.y = p32.y; r.z = p32.z; r.path = p;
+                const int64_t row = (int64_t)(cnt + rank) * nq + j;
+                st_row(&m.in[row], r);
+                if (write_k) m.sk[row] = kk;
+            }
+            const int32_t n_ev = __popc(bal);
+            if (cnt + n_ev >= budget) {
+                // budget filled: resume after the last candidate taken
+                uint32_t b = bal;
+                for (int32_t t = 1; t < budget - cnt; ++t) b &= b - 1u;
+                k += __ffs(b);
+                cnt = budget;
+                break;
+            }
+            cnt += n_ev;
+            const int32_t last = min(G, sg.n - k) - 1;     // last candidate tested
+            int32_t knext = k + last + 1;
+            // an empty cell at the last candidate: skip the rest of it (gen_path's DDA)
+            const bool last_ins = g.bcast((int32_t)ins, (uint32_t)last) != 0;
+            if (last_ins && !((bal >> last) & 1u)) {
+                int32_t kj = 0;
+                if ((int32_t)g.gl == last) kj = dda_next(nf, fld, of, df, sg, kk, cell3);
+                knext = max(knext, g.bcast(kj, (uint32_t)last));
+            }
+            k = knext;
+        }
+    }
+    for (int32_t i = cnt + (int32_t)g.gl; i < S; i += G) {
+        fws::SampleIn r;
+        r.x = r.y = r.z = 0.f;
+        r.path = -1;
+        st_row(&m.in[(int64_t)i * nq + j], r);
+    }
+    if (g.gl == 0) {
+        m.cnt[p] = cnt;
+        m.k[p] = k;
+    }
+    return cnt;
+}
+
+// One tail round of k_step<true>, G lanes per queued path.
+template <int G>
+HRT_DEV void step_tail(const Args& a, const MarchState& m, int32_t first, int32_t S, int32_t prev_nq,
+                       int32_t nq, const int32_t* q, int32_t* next, int32_t* next_n, int32_t& done,
+                       int32_t& made, int32_t& held, int32_t& segs) {
+    const PathState& s = a.ps;
+    const Grp<G> g;
+    const int32_t groups = (int32_t)(gridDim.x * blockDim.x / G);
+    for (int32_t j = (int32_t)((blockIdx.x * blockDim.x + threadIdx.x) / G); j < nq; j += groups) {
+        const int32_t p = q[j];
+        Acc c;
+        load_acc(s, p, c);
+        int32_t go = 1;
+        if (!first) {
+            const bool stop = a.sc.em.n > 0
+                                  ? comp_path_tail<G, true>(a, m, m.base[p], prev_nq, m.cnt[p], m.delta[p], c, done, g)
+                                  : comp_path_tail<G, false>(a, m, m.base[p], prev_nq, m.cnt[p], m.delta[p], c, done, g);
+            if (g.gl == 0) go = !stop && !halted(a.sc, c) && m.k[p] < m.n[p];
+        } else if (g.gl == 0) {
+            go = m.k[p] < m.n[p];
+        }
+        int32_t neval = 0, halt = 0;
+        if (g.gl == 0) {
+            if (!go) go = advance(a, m, p, c, segs);
+            store_acc(s, p, c);
+            neval = c.neval;
+            halt = halted(a.sc, c);
+        }
+        __syncwarp(g.gmask);                     // lane 0's path-state writes -> the group
+        go = g.bcast(go, 0);
+        if (go) {
+            neval = g.bcast(neval, 0);
+            halt = g.bcast(halt, 0);
+            int32_t r = 0;
+            if (g.gl == 0) {
+                r = reserve(next_n);
+                next[r] = p;
+                m.base[p] = r;
+            }
+            r = g.bcast(r, 0);
+            const int32_t cnt = gen_path_tail<G>(a, m, p, r, nq, S, neval, halt != 0, g);
+            if (g.gl == 0) {
+                made += cnt;
+                ++held;
+            }
+        }
+    }
+}
+
 #ifndef HRT_STEP_MINB
 #define HRT_STEP_MINB 3
 #endif
@@ -672,6 +854,9 @@ __global__ void __launch_bounds__(256, HRT_STEP_MINB) k_step(Args a, MarchState 
     int32_t* next_n = &a.ps.counters[C_MQ0 + (mcur ^ 1)];
     const PathState& s = a.ps;
     int32_t done = 0, made = 0, held = 0, segs = 0;
+    if (kMixed && kTailLanes > 1 && ctr[C_TAIL]) {
+        step_tail<kTailLanes>(a, m, first, S, prev_nq, nq, q, next, next_n, done, made, held, segs);
+    } else
     for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += gridDim.x * blockDim.x) {
         const int32_t p = q[j];
         Acc c;
@@ -916,6 +1101,7 @@ __global__ void k_round_begin(int32_t* c, unsigned long long* stats, int32_t tar
         S = max(1, min(S, batch_cap / live));
     }
     c[C_S] = S;
+    c[C_TAIL] = live > 0 && live < kTailLive;
     c[C_PSTRIDE] = c[C_STRIDE];
     c[C_STRIDE] = live;
     c[C_MQ0 + (cur ^ 1)] = 0;
