@@ -900,7 +900,11 @@ __global__ void __launch_bounds__(256, HRT_STEP_MINB) k_step(Args a, MarchState 
 // traces the shadow rays of 32 neighbouring pixels at the same step). Rows
 // that cannot contribute (opacity 0 or black) cast no ray, as in the
 // reference (field.py:246-251).
-__global__ void k_shadow(Args a, MarchState m, fws::RowMap rm, int64_t rows, int32_t dev_rows) {
+#ifndef HRT_SHADOW_MINB
+#define HRT_SHADOW_MINB 4
+#endif
+__global__ void __launch_bounds__(256, HRT_SHADOW_MINB) k_shadow(Args a, MarchState m, fws::RowMap rm, int64_t rows,
+                                                             int32_t dev_rows) {
     const PathState& s = a.ps;
     if (dev_rows) {                  // device-driven round: this round's batch shape
         const int32_t* ctr = a.ps.counters;
@@ -960,7 +964,10 @@ constexpr bool kShadowOrdered = HRT_SHADOW_ORDERED;
 #endif
 constexpr int kRefillLanes = HRT_REFILL_LANES;    // idle lanes that trigger a warp refill
 
-__global__ void __launch_bounds__(256) k_shadow_trace(Args a, MarchState m) {
+#ifndef HRT_SHTRACE_MINB
+#define HRT_SHTRACE_MINB 4
+#endif
+__global__ void __launch_bounds__(256, HRT_SHTRACE_MINB) k_shadow_trace(Args a, MarchState m) {
     const int32_t n = a.ps.counters[C_SHQ];
     int32_t* fetch = &a.ps.counters[C_SHF];
     const DevBvh& b = a.sc.blockers;
