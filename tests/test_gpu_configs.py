@@ -169,7 +169,7 @@ def test_gpu_rigid_refit_equals_host_moved_scene():
     r.close()
 
 
-@pytest.mark.parametrize("which", ["cfg1", "shadows", "cfg2", "moving"])
+@pytest.mark.parametrize("which", ["cfg1", "cfg1_full", "shadows", "cfg2", "moving"])
 def test_gpu_continuous_march_equals_bounce_loop(cuda, which):
     """The continuous wavefront march (paths advance to their next bounce
     inside the march rounds, kern::advance) against the reference's
@@ -177,6 +177,8 @@ def test_gpu_continuous_march_equals_bounce_loop(cuda, which):
     sample counts, shadow rays and bounce rays are identical, bit for bit."""
     if which == "cfg1":
         scene, spp, size, cx, cy = configs.cfg1(), 1, 48, 400, 400
+    elif which == "cfg1_full":          # 640 k paths: wide rounds first, 8-lane tail rounds last
+        scene, spp, size, cx, cy = configs.cfg1(), 1, None, None, None
     elif which == "shadows":
         scene, spp, size, cx, cy = shadow_scene(), 4, 16, 32, 20
     elif which == "cfg2":
@@ -185,7 +187,8 @@ def test_gpu_continuous_march_equals_bounce_loop(cuda, which):
         scene, spp, size, cx, cy = moving_scene(3), 2, 32, 48, 32
     r = Renderer(scene)
     w, h = scene.camera.resolution
-    pix = torch.as_tensor(crop(w, h, size, cx=cx, cy=cy).astype(np.int32), device=cuda)
+    pix = None if size is None else torch.as_tensor(crop(w, h, size, cx=cx, cy=cy).astype(np.int32),
+                                                     device=cuda)
     out = {}
     for continuous in (True, False):
         r.set_march(continuous)
