@@ -154,22 +154,30 @@ struct Ray32 {
     float ox, oy, oz, ix, iy, iz;
 };
 
+// Reciprocal direction with |d| < 1e-30 (zero included) taken as +-1e-30:
+// the slab products then never form 0 * inf = NaN, so the box test needs no
+// NaN handling. Still conservative: such a ray parallel to a slab gets an
+// interval of +-1e30-scale t (the whole axis when its origin is inside the
+// slab, far outside the scene when it is not), as the exact reciprocal would.
+HRT_DEV float rcp_safe(double dd) {
+    const float f = (float)dd;
+    return 1.0f / (fabsf(f) < 1e-30f ? copysignf(1e-30f, f) : f);
+}
+
 HRT_DEV Ray32 prep32(d3 o, d3 d) {
     Ray32 r;
     r.ox = (float)o.x; r.oy = (float)o.y; r.oz = (float)o.z;
-    r.ix = 1.0f / (float)d.x; r.iy = 1.0f / (float)d.y; r.iz = 1.0f / (float)d.z;
+    r.ix = rcp_safe(d.x); r.iy = rcp_safe(d.y); r.iz = rcp_safe(d.z);
     return r;
 }
 
 HRT_DEV float t_lo32(double t) { return t <= 0.0 ? (float)t * 1.00001f - 1e-5f : (float)t * 0.99999f - 1e-5f; }
 HRT_DEV float t_hi32(double t) { return (float)t * 1.00001f + 1e-5f; }
 
-// NaN (0 * inf: axis-aligned ray on a slab plane) widens to the whole axis.
 HRT_DEV void slab_axis(float lo, float hi, float o, float inv, float& tn, float& tf) {
-    const float ta = (lo - o) * inv, tb = (hi - o) * inv;
-    const bool nan = (ta != ta) || (tb != tb);
-    tn = fmaxf(tn, nan ? -INFINITY : fminf(ta, tb));
-    tf = fminf(tf, nan ? INFINITY : fmaxf(ta, tb));
+    const float ta = (lo - o) * inv, tb = (hi - o) * inv;     // finite inv: no NaN (rcp_safe)
+    tn = fmaxf(tn, fminf(ta, tb));
+    tf = fminf(tf, fmaxf(ta, tb));
 }
 
 HRT_DEV bool box32(float lx, float ly, float lz, float hx, float hy, float hz, const Ray32& r,
