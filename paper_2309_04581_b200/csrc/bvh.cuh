@@ -367,19 +367,22 @@ HRT_DEV int32_t closest_q(const DevBvh& b, d3 o, d3 d, double t_min, double t_ma
     float stack_t[kStackQ];
     int sp = 0;
     int32_t cur = 0;
+    float lim = t_hi32(t_max);        // t_hi32(min(t_max, best_t)), refreshed when a leaf hits
     while (true) {
         const QNode q = load_q(b, cur);
         float nr[4];
-        uint32_t m = qchildren(q, r, t0, t_hi32(fmin(t_max, best_t)), nr);
+        uint32_t m = qchildren(q, r, t0, lim, nr);
         // leaves first (they can only shrink best_t)
+        const uint32_t leaves = m & ((qref(q, 0) < 0 ? 1u : 0u) | (qref(q, 1) < 0 ? 2u : 0u) |
+                                     (qref(q, 2) < 0 ? 4u : 0u) | (qref(q, 3) < 0 ? 8u : 0u));
+        if (leaves) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if ((m >> k & 1u) && qref(q, k) < 0) {
-                leaf_closest(b, qref(q, k), o, d, t_min, t_max, best_t, best_f);
-                m &= ~(1u << k);
-            }
+            for (int k = 0; k < 4; ++k)
+                if (leaves >> k & 1u) leaf_closest(b, qref(q, k), o, d, t_min, t_max, best_t, best_f);
+            m &= ~leaves;
+            lim = t_hi32(fmin(t_max, best_t));
+        }
         // inner children: nearest next, the rest pushed far-to-near
-        const float lim = t_hi32(fmin(t_max, best_t));
         int32_t next = -1;
         while (m) {
             int kb = -1;
@@ -394,10 +397,9 @@ HRT_DEV int32_t closest_q(const DevBvh& b, d3 o, d3 d, double t_min, double t_ma
         }
         if (next >= 0) { cur = next; continue; }
         bool found = false;
-        const float lim2 = t_hi32(fmin(t_max, best_t));
         while (sp > 0) {
             --sp;
-            if (stack_t[sp] <= lim2) { cur = stack[sp]; found = true; break; }
+            if (stack_t[sp] <= lim) { cur = stack[sp]; found = true; break; }
         }
         if (!found) break;
     }
