@@ -106,6 +106,14 @@ HRT_DEV float corner_weight(const LevelCoord& c, int corner) {
 constexpr bool kPairGathers = HRT_PAIR_GATHERS;
 
 // acc (two packed fp32) = fma(w, v, acc) per lane of the pair: one FFMA2.
+// (a.x * b.x, a.y * b.y), each rounded as a scalar FMUL: one FMUL2.
+HRT_DEV float2 mul2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r)
+        : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+    return *reinterpret_cast<float2*>(&r);
+}
+
 HRT_DEV void fma2(float2& acc, float w, float2 v) {
     unsigned long long a = *reinterpret_cast<unsigned long long*>(&acc);
     const unsigned long long b = *reinterpret_cast<const unsigned long long*>(&v);
@@ -270,17 +278,37 @@ HRT_DEV void level_issue(const NeuralField& nf, const NeuralLevel& lv, float3 re
     }
 }
 
+#ifndef HRT_PACKED_WEIGHTS
+#define HRT_PACKED_WEIGHTS 1
+#endif
 template <int F = 2>
 HRT_DEV void level_finish(const LevelLoadsF<F>& g, float* out) {
     const LevelCoord& c = g.c;
     const float gx = __fsub_rn(1.0f, c.f[0]), gy = __fsub_rn(1.0f, c.f[1]),
                 gz = __fsub_rn(1.0f, c.f[2]);
-    const float wxy[4] = {__fmul_rn(gx, gy), __fmul_rn(c.f[0], gy), __fmul_rn(gx, c.f[1]),
-                          __fmul_rn(c.f[0], c.f[1])};
+    // wxy = (gx gy, fx gy, gx fy, fx fy); corner k weight = wxy[k & 3] * (gz | fz),
+    // formed as FMUL2 pairs (each lane rounded as a scalar FMUL)
+    float wxy[4], w[8];
+    if (HRT_PACKED_WEIGHTS) {
+        const float2 x2 = make_float2(gx, c.f[0]);
+        const float2 a = mul2(x2, make_float2(gy, gy)), b = mul2(x2, make_float2(c.f[1], c.f[1]));
+        wxy[0] = a.x; wxy[1] = a.y; wxy[2] = b.x; wxy[3] = b.y;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float2 p = mul2(make_float2(wxy[k], wxy[k]), make_float2(gz, c.f[2]));
+            w[k] = p.x;
+            w[k + 4] = p.y;
+        }
+    } else {
+        wxy[0] = __fmul_rn(gx, gy); wxy[1] = __fmul_rn(c.f[0], gy);
+        wxy[2] = __fmul_rn(gx, c.f[1]); wxy[3] = __fmul_rn(c.f[0], c.f[1]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[k] = __fmul_rn(wxy[k & 3], (k & 4) ? c.f[2] : gz);
+    }
     if constexpr (F == 2) {
         float2 acc[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
 #pragma unroll
-        for (int k = 0; k < 8; ++k) fma2(acc[k & 1], __fmul_rn(wxy[k & 3], (k & 4) ? c.f[2] : gz), g.v[k]);
+        for (int k = 0; k < 8; ++k) fma2(acc[k & 1], w[k], g.v[k]);
         out[0] = __fadd_rn(acc[0].x, acc[1].x);
         out[1] = __fadd_rn(acc[0].y, acc[1].y);
     } else {
@@ -289,9 +317,8 @@ HRT_DEV void level_finish(const LevelLoadsF<F>& g, float* out) {
         float2 a1[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const float w = __fmul_rn(wxy[k & 3], (k & 4) ? c.f[2] : gz);
-            fma2(a0[k & 1], w, make_float2(g.v[k].x, g.v[k].y));
-            fma2(a1[k & 1], w, make_float2(g.v[k].z, g.v[k].w));
+            fma2(a0[k & 1], w[k], make_float2(g.v[k].x, g.v[k].y));
+            fma2(a1[k & 1], w[k], make_float2(g.v[k].z, g.v[k].w));
         }
         out[0] = __fadd_rn(a0[0].x, a0[1].x); out[1] = __fadd_rn(a0[0].y, a0[1].y);
         out[2] = __fadd_rn(a1[0].x, a1[1].x); out[3] = __fadd_rn(a1[0].y, a1[1].y);
