@@ -265,6 +265,31 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def open_peer_frame(w, h, rank, world):
+    """PeerFrame (rank 0's frame mapped into every rank with CUDA IPC), or None
+    on every rank if any rank cannot map it (then the frame is assembled with
+    the NCCL all-gather instead): the ranks agree before the first frame."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2309_04581_b200.tiles import PeerFrame
+    peer, ok = None, 1
+    try:
+        peer = PeerFrame(w, h, rank, world)
+    except Exception as e:        # noqa: BLE001 - any IPC failure -> the NCCL path
+        print(f"rank {rank}: peer-memory frame unavailable ({e}); using the NCCL all-gather",
+              file=sys.stderr, flush=True)
+        ok = 0
+    if world > 1:
+        flag = torch.tensor([ok], dtype=torch.int32, device=torch.cuda.current_device())
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        ok = int(flag.item())
+    if not ok and peer is not None:
+        peer.close(barrier=False)         # (no frame was rendered into it)
+        peer = None
+    return peer
+
+
 def run_ours(args, rank, world, local):
     import numpy as np
     import torch
@@ -295,7 +320,7 @@ def run_ours(args, rank, world, local):
     n_local = len(pix_host)
     gather = FrameGather(w, h, rank, world, dev)
     out = gather.local
-    peer = PeerFrame(w, h, rank, world) if args.gather == "peer" else None
+    peer = open_peer_frame(w, h, rank, world) if args.gather == "peer" else None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 

@@ -109,19 +109,29 @@ class PeerFrame:
         self.lib = _lib.load()
         self._owner = rank == 0
         p = ctypes.c_void_p()
+        self.ptr = None
+        err = None
+        blob = [None]
         if self._owner:
-            _lib.check(self.lib.hrt_buffer_alloc(w * h * 3 * 8, ctypes.byref(p)), "hrt_buffer_alloc")
-            hd = (ctypes.c_uint8 * 64)()
-            _lib.check(self.lib.hrt_ipc_handle(p, hd), "hrt_ipc_handle")
-            blob = [bytes(hd)]
-        else:
-            blob = [None]
+            try:
+                _lib.check(self.lib.hrt_buffer_alloc(w * h * 3 * 8, ctypes.byref(p)), "hrt_buffer_alloc")
+                self.ptr = p.value
+                hd = (ctypes.c_uint8 * 64)()
+                _lib.check(self.lib.hrt_ipc_handle(p, hd), "hrt_ipc_handle")
+                blob = [bytes(hd)]
+            except Exception as e:        # noqa: BLE001 - every rank must still reach the broadcast
+                err = e
         if world > 1:
             dist.broadcast_object_list(blob, src=0, group=group)
-        if not self._owner:
+        if not self._owner and blob[0] is not None:
             hd = (ctypes.c_uint8 * 64).from_buffer_copy(blob[0])
             _lib.check(self.lib.hrt_ipc_open(hd, ctypes.byref(p)), "hrt_ipc_open")
-        self.ptr = p.value
+            self.ptr = p.value
+        if blob[0] is None:
+            if self._owner and self.ptr is not None:
+                self.lib.hrt_buffer_free(self.ptr)
+                self.ptr = None
+            raise RuntimeError(f"rank 0 could not export its frame: {err}")
 
     def done(self):
         import torch
@@ -142,11 +152,11 @@ class PeerFrame:
         from .renderer import finalize_device
         return finalize_device(self.frame(), self.w, self.h, hdr_output).cpu().numpy().tobytes()
 
-    def close(self):
+    def close(self, barrier=True):
         import torch.distributed as dist
         if self.ptr is None:
             return
-        if self.world > 1:
+        if self.world > 1 and barrier:
             dist.barrier(group=self.group)        # no rank still writes into rank 0's frame
         if self._owner:
             self.lib.hrt_buffer_free(self.ptr)
