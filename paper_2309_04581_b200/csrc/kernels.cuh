@@ -675,7 +675,7 @@ HRT_DEV bool advance(const Args& a, const MarchState& m, int32_t p, Acc& c, int3
 #define HRT_TAIL_LANES 8
 #endif
 #ifndef HRT_TAIL_LIVE
-#define HRT_TAIL_LIVE 16384
+#define HRT_TAIL_LIVE 2048
 #endif
 constexpr int kTailLanes = HRT_TAIL_LANES;
 constexpr int kTailLive = HRT_TAIL_LIVE;      // k_round_begin: tail mode below this many paths
