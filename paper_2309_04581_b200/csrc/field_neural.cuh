@@ -1,13 +1,8 @@
-// field_neural.cuh - K5 hash-grid encode, K6 fused density/SH/colour MLP on
-// tcgen05, occupancy lookups (CPU definition in
-// oracle/field.py).
-//
-// CTA model: 128 threads = 128 MMA rows (M = 128). Each thread owns one
-// sample: it gathers its hash-grid features straight into its row of the
-// smem A operand (fp16), then the CTA runs the five layers as UMMAs whose
-// fp32 accumulators land in TMEM; thread t reads back TMEM lane t with
-// tcgen05.ld, applies the activation in registers and writes the next
-// layer's A row. Weights stay resident in smem for the whole kernel.
+// field_neural.cuh - the neural field's building blocks (SURVEY Appendix B
+// P1-P4; CPU definition in oracle/field.py): hash-grid level coordinates,
+// corner indices and the two-phase gather/accumulate the field engine
+// (field_ws.cuh) runs per level, SH(16), output activations, occupancy
+// lookups, and the packed-weight layout of the tcgen05 MLP.
 #pragma once
 #include <cuda_fp16.h>
 #include "common.cuh"
@@ -15,9 +10,6 @@
 
 namespace nerf {
 
-constexpr int kRows = 128;
-constexpr int kTmemCols = 128;       // [0,64): 64-wide outputs, [64,80): 16-wide
-constexpr int kAStride = 64;         // A buffer holds up to K = 64 halves per row
 constexpr uint32_t kHashY = 2654435761u, kHashZ = 805459861u;
 
 // Byte offsets of the packed layers inside NeuralField::wpack (host packs
@@ -29,42 +21,8 @@ __host__ __device__ constexpr WOff woff(int E) {
             (uint32_t)(64 * E * 2 + 2048 + 4096 + 8192 + 2048)};
 }
 
-struct SmemLayout {
-    uint32_t w, a, mbar, tslot, total;
-};
-__host__ __device__ constexpr SmemLayout smem_layout(int E) {
-    // weights | A (128 x 64 fp16) | mbarrier | tmem address slot
-    return {0u, woff(E).total, woff(E).total + 16384u, woff(E).total + 16384u + 8u,
-            woff(E).total + 16384u + 16u};
-}
-
 // ------------------------------------------------------------- encode (K5)
 HRT_DEV float3 to_f32(d3 p) { return make_float3((float)p.x, (float)p.y, (float)p.z); }
-
-// Store 8 consecutive features [k0, k0+8) of row m as fp16 (round to nearest).
-HRT_DEV void store8(uint8_t* A, int m, int k0, int K, const float* v) {
-    __half2 h[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
-    *reinterpret_cast<uint4*>(A + umma::layout_offset(m, k0, K)) = *reinterpret_cast<uint4*>(h);
-}
-
-// Store 4 consecutive features [k0, k0+4) (k0 % 4 == 0) of row m as fp16.
-HRT_DEV void store4(uint8_t* A, int m, int k0, int K, const float* v) {
-    __half2 h[2] = {__floats2half2_rn(v[0], v[1]), __floats2half2_rn(v[2], v[3])};
-    *reinterpret_cast<uint2*>(A + umma::layout_offset(m, k0, K)) = *reinterpret_cast<uint2*>(h);
-}
-
-// Store n (4, 8 or 16) consecutive features starting at k0.
-template <int N>
-HRT_DEV void store_n(uint8_t* A, int m, int k0, int K, const float* v) {
-    if constexpr (N == 4) {
-        store4(A, m, k0, K, v);
-    } else {
-#pragma unroll
-        for (int k = 0; k < N; k += 8) store8(A, m, k0 + k, K, v + k);
-    }
-}
 
 struct LevelCoord {
     int32_t i[3];
@@ -91,13 +49,6 @@ HRT_DEV uint32_t corner_index(const NeuralLevel& lv, const LevelCoord& c, int co
     const uint32_t Z = (uint32_t)c.i[2] + (corner >> 2);
     if (lv.dense) return X + lv.r * Y + lv.r * lv.r * Z;
     return (X ^ (Y * kHashY) ^ (Z * kHashZ)) & tmask;
-}
-
-HRT_DEV float corner_weight(const LevelCoord& c, int corner) {
-    const float wx = (corner & 1) ? c.f[0] : __fsub_rn(1.0f, c.f[0]);
-    const float wy = ((corner >> 1) & 1) ? c.f[1] : __fsub_rn(1.0f, c.f[1]);
-    const float wz = (corner >> 2) ? c.f[2] : __fsub_rn(1.0f, c.f[2]);
-    return __fmul_rn(__fmul_rn(wx, wy), wz);
 }
 
 #ifndef HRT_PAIR_GATHERS
@@ -331,27 +282,6 @@ HRT_DEV float3 rel_coord(const NeuralField& nf, d3 pf) {
                        __fsub_rn(p.z, nf.lo32[2]));
 }
 
-// Encode row m of the A operand (E = L*F halves); zero row when !valid.
-template <int E, int F>
-HRT_DEV void encode_row(const NeuralField& nf, d3 pf, bool valid, uint8_t* A, int m) {
-    constexpr int L = E / F;
-    constexpr int kPerChunk = 8 / F;     // levels per 16-byte chunk
-    const float3 rel = rel_coord(nf, pf);
-#pragma unroll
-    for (int l0 = 0; l0 < L; l0 += kPerChunk) {
-        float v[8];
-#pragma unroll
-        for (int j = 0; j < kPerChunk; ++j) {
-            if (valid) encode_level<F>(nf, nf.lv[l0 + j], rel, v + j * F);
-            else {
-#pragma unroll
-                for (int q = 0; q < F; ++q) v[j * F + q] = 0.0f;
-            }
-        }
-        store8(A, m, l0 * F, E, v);
-    }
-}
-
 // ------------------------------------------------------------ occupancy
 HRT_DEV int32_t occ_cell(const NeuralField& nf, d3 pf, int32_t c[3]) {
     const float3 rel = rel_coord(nf, pf);
@@ -387,128 +317,9 @@ HRT_DEV void sh16(float x, float y, float z, float* o) {
     o[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
 }
 
-// ------------------------------------------------------------ MLP (K6)
-struct Tile {
-    uint8_t* A;          // generic pointer to the A operand buffer
-    uint32_t a_addr;     // its shared-window address
-    uint32_t w_addr;     // packed weights
-    uint32_t mbar;
-    uint32_t tmem;
-    uint32_t phase;
-    uint32_t lane_base;  // (warp & 3) * 32, TMEM lane quarter of this warp
-};
-
-// Thread 0 issues D[tmem_col] = A(128 x K) * B(N x K)^T as K/16 UMMAs and
-// commits them to the mbarrier.
-HRT_DEV void issue(const Tile& t, uint32_t tmem_col, int K, uint32_t b_addr, int N) {
-    if (threadIdx.x == 0) {
-        umma::fence_after();
-        const uint32_t id = umma::idesc_f16(kRows, N);
-        for (int s = 0; s < K / 16; ++s) {
-            const uint64_t a = umma::desc(t.a_addr + s * 256, K * 16);
-            const uint64_t b = umma::desc(b_addr + s * 256, K * 16);
-            umma::mma_f16(t.tmem + tmem_col, a, b, id, s > 0 ? 1u : 0u);
-        }
-        umma::commit(t.mbar);
-    }
-}
-
-// Publish A rows (all threads wrote theirs), run one layer, wait for it.
-HRT_DEV void run_layer(Tile& t, uint32_t tmem_col, int K, uint32_t b_off, int N) {
-    umma::fence_async_smem();
-    umma::fence_before();
-    __syncthreads();
-    issue(t, tmem_col, K, t.w_addr + b_off, N);
-    umma::mbar_wait(t.mbar, t.phase);
-    t.phase ^= 1u;
-    umma::fence_after();
-}
-
-HRT_DEV void relu_store64(Tile& t, const float* v) {
-    const int m = threadIdx.x;
-#pragma unroll
-    for (int k0 = 0; k0 < 64; k0 += 8) {
-        float r[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) r[i] = fmaxf(v[k0 + i], 0.0f);
-        store8(t.A, m, k0, 64, r);
-    }
-}
-
 HRT_DEV float out_act(float x, int act) {
     if (act == 0) return 1.0f / (1.0f + expf(-x));
     return x > 20.0f ? x : log1pf(expf(x));
-}
-
-// Layers after the encode: A already holds the encoded rows (K = E).
-// Returns sigma; rgb unless density_only.
-template <int E>
-HRT_DEV float mlp(Tile& t, const NeuralField& nf, float3 dir, bool density_only, float* rgb) {
-    constexpr WOff W = woff(E);
-    const uint32_t lane = t.lane_base << 16;
-    float h[64];
-    run_layer(t, 0, E, W.d1, 64);                      // density hidden
-    umma::ld64(t.tmem + lane + 0, h);
-    relu_store64(t, h);
-    run_layer(t, 64, 64, W.d2, 16);                    // density head
-    float o[16];
-    umma::ld16(t.tmem + lane + 64, o);
-    const float sigma = expf(o[0]);
-    if (density_only) return sigma;
-    float c[32];
-    sh16(dir.x, dir.y, dir.z, c);
-#pragma unroll
-    for (int i = 1; i < 16; ++i) c[15 + i] = o[i];
-    c[31] = 0.0f;
-#pragma unroll
-    for (int k0 = 0; k0 < 32; k0 += 8) store8(t.A, threadIdx.x, k0, 32, c + k0);
-    run_layer(t, 0, 32, W.c1, 64);                     // colour hidden 1
-    umma::ld64(t.tmem + lane + 0, h);
-    relu_store64(t, h);
-    run_layer(t, 0, 64, W.c2, 64);                     // colour hidden 2
-    umma::ld64(t.tmem + lane + 0, h);
-    relu_store64(t, h);
-    run_layer(t, 64, 64, W.c3, 16);                    // colour head (3 of 16 used)
-    umma::ld16(t.tmem + lane + 64, o);
-    rgb[0] = out_act(o[0], nf.act);
-    rgb[1] = out_act(o[1], nf.act);
-    rgb[2] = out_act(o[2], nf.act);
-    return sigma;
-}
-
-// CTA prologue: copy packed weights to smem, allocate TMEM, init mbarrier.
-template <int E>
-HRT_DEV Tile tile_setup(const NeuralField& nf, uint8_t* smem) {
-    constexpr SmemLayout S = smem_layout(E);
-    constexpr WOff W = woff(E);
-    const uint4* src = reinterpret_cast<const uint4*>(nf.wpack);
-    uint4* dst = reinterpret_cast<uint4*>(smem + S.w);
-    for (uint32_t i = threadIdx.x; i < W.total / 16; i += blockDim.x) dst[i] = __ldg(src + i);
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + S.tslot);
-    if (threadIdx.x < 32) umma::tmem_alloc(umma::saddr(tslot), kTmemCols);
-    if (threadIdx.x == 0) {
-        umma::mbar_init(umma::saddr(smem + S.mbar), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    umma::fence_async_smem();
-    umma::fence_before();
-    __syncthreads();
-    umma::fence_after();
-    Tile t;
-    t.A = smem + S.a;
-    t.a_addr = umma::saddr(smem + S.a);
-    t.w_addr = umma::saddr(smem + S.w);
-    t.mbar = umma::saddr(smem + S.mbar);
-    t.tmem = *tslot;
-    t.phase = 0;
-    t.lane_base = (threadIdx.x >> 5) * 32;
-    return t;
-}
-
-HRT_DEV void tile_teardown(const Tile& t) {
-    umma::fence_before();
-    __syncthreads();
-    if (threadIdx.x < 32) umma::tmem_free(t.tmem, kTmemCols);
 }
 
 }  // namespace nerf
