@@ -1,7 +1,14 @@
-// kernels.cuh - the wavefront render pipeline (one chunk of camera paths):
-//   k_raygen -> per bounce { k_intersect -> k_march_* -> k_shade } -> k_accumulate
-// Path state is SoA in HBM; the alive set is a ping-pong index queue whose
-// length lives on the device, so a whole frame launches without host syncs.
+// kernels.cuh - the wavefront render pipeline (one chunk of camera paths).
+// Neural field, hybrid mode (the continuous march, default):
+//   k_raygen -> k_paths (every bounce's ray + nearest hit) -> k_seg ->
+//   rounds of { k_round_begin -> k_step (composite, shade/advance, generate)
+//               -> fws::k_field_ws -> [k_shadow -> k_shadow_trace] } -> k_accumulate
+// Other fields / modes, and the reference's bounce-by-bounce schedule:
+//   k_raygen -> per bounce { k_intersect -> march (dense: k_march_dense) -> k_shade }
+//   -> k_accumulate
+// Path state is SoA in HBM; the alive sets are ping-pong index queues whose
+// lengths live on the device, so rounds launch without host syncs (the host
+// checks for completion every few rounds).
 #pragma once
 #include <cooperative_groups.h>
 #include "bvh.cuh"
