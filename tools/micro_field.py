@@ -1,5 +1,5 @@
 """Microbenchmark of the field kernels on ray-coherent sample streams:
-hash encode alone (k_field_encode) vs encode + tcgen05 MLP (k_field_eval)."""
+hash encode alone (hrt_field_encode) vs encode + tcgen05 MLP (hrt_field_sample, the field engine)."""
 import sys
 
 import numpy as np
