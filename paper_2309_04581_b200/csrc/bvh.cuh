@@ -406,6 +406,89 @@ HRT_DEV int32_t closest_q(const DevBvh& b, d3 o, d3 d, double t_min, double t_ma
     return best_f;
 }
 
+// Nearest hit with 4 lanes per ray (a group of 4 consecutive lanes, gl = lane
+// in group): lane k tests child k of the current node - its box and, for a
+// leaf child, its triangles - and the group combines the results by shuffles.
+// For the latency-bound case (few rays, long traversals): a node visit costs
+// one box test and one leaf test instead of four of each. Every lane keeps
+// the same traversal state. The answer is the lexicographic minimum (t, face)
+// over the triangles whose boxes the ray reaches, as closest_q's.
+HRT_DEV int32_t closest_q_coop(const DevBvh& b, d3 o, d3 d, double t_min, double t_max, double& best_t,
+                               uint32_t gmask, uint32_t gbase, uint32_t gl) {
+    best_t = INFINITY;
+    int32_t best_f = -1;
+    if (b.n_faces == 0) return -1;
+    const Ray32 r = prep32(o, d);
+    const float t0 = t_lo32(t_min);
+    float lim = t_hi32(t_max);
+    int32_t stack[kStackQ];
+    float stack_t[kStackQ];
+    int sp = 0;
+    int32_t cur = 0;
+    while (true) {
+        const float* q = reinterpret_cast<const float*>(b.qnodes + cur);
+        const float lx = __ldg(q + gl), ly = __ldg(q + 4 + gl), lz = __ldg(q + 8 + gl);
+        const float hx = __ldg(q + 12 + gl), hy = __ldg(q + 16 + gl), hz = __ldg(q + 20 + gl);
+        const int32_t ref = __ldg(reinterpret_cast<const int32_t*>(q) + 24 + gl);
+        float nr;
+        const bool hit = box32(lx, ly, lz, hx, hy, hz, r, t0, lim, nr);
+        // leaf child of this lane
+        double lt = INFINITY;
+        int32_t lf = 0x7fffffff;
+        if (hit && ref < 0) {
+            const int32_t code = ~ref, first = code >> 3, count = code & 7;
+            for (int i = 0; i < count; ++i) {
+                const int32_t li = first + i;
+                const double t = moller_trumbore(o, d, b.tri + 9 * (size_t)li, t_min, t_max);
+                if (t < INFINITY) {
+                    const int32_t f = b.tri_id[li];
+                    if (t < lt || (t == lt && f < lf)) { lt = t; lf = f; }
+                }
+            }
+        }
+        const uint32_t leaves = (__ballot_sync(gmask, hit && ref < 0) >> gbase) & 0xFu;
+        if (leaves) {
+#pragma unroll
+            for (int off = 1; off < 4; off <<= 1) {
+                const double ot = __shfl_xor_sync(gmask, lt, off);
+                const int32_t of = __shfl_xor_sync(gmask, lf, off);
+                if (ot < lt || (ot == lt && of < lf)) { lt = ot; lf = of; }
+            }
+            if (lt < best_t || (lt == best_t && lf < best_f)) { best_t = lt; best_f = lf; }
+            lim = t_hi32(fmin(t_max, best_t));
+        }
+        // inner children: nearest next, the rest pushed far-to-near (as closest_q)
+        uint32_t m = (__ballot_sync(gmask, hit && ref >= 0) >> gbase) & 0xFu;
+        float nr4[4];
+        int32_t ref4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            nr4[k] = __shfl_sync(gmask, nr, (int)(gbase + k));
+            ref4[k] = __shfl_sync(gmask, ref, (int)(gbase + k));
+        }
+        int32_t next = -1;
+        while (m) {
+            int kb = -1;
+            float tb = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if ((m >> k & 1u) && nr4[k] >= tb) { tb = nr4[k]; kb = k; }
+            m &= ~(1u << kb);
+            if (tb > lim) continue;
+            if (m == 0) { next = ref4[kb]; break; }
+            if (sp < kStackQ) { stack[sp] = ref4[kb]; stack_t[sp] = tb; ++sp; }
+        }
+        if (next >= 0) { cur = next; continue; }
+        bool found = false;
+        while (sp > 0) {
+            --sp;
+            if (stack_t[sp] <= lim) { cur = stack[sp]; found = true; break; }
+        }
+        if (!found) break;
+    }
+    return best_f;
+}
+
 // True if any face lies in (t_min, t_max] (surface.py:442-478), 4-wide tree.
 HRT_DEV bool any_hit_q(const DevBvh& b, d3 o, d3 d, double t_min, double t_max) {
     if (b.n_faces == 0) return false;

@@ -58,6 +58,10 @@ constexpr int kTexLevels = HRT_TEX_LEVELS;        // finest levels gathered via 
 #define HRT_MIXED_MARCH 1
 #endif
 constexpr bool kMixedMarch = HRT_MIXED_MARCH;     // continuous wavefront march (kern::advance)
+#ifndef HRT_COOP_PATHS
+#define HRT_COOP_PATHS 200000
+#endif
+constexpr int64_t kCoopPaths = HRT_COOP_PATHS;     // k_paths_coop (4 lanes per path) below this
 #ifndef HRT_TILED_FRAME
 #define HRT_TILED_FRAME 1
 #endif
@@ -1068,7 +1072,8 @@ int run_bounces(hrt_handle* h, kern::Args& a, int64_t paths, int mode, cudaStrea
         if ((rc = ensure_geo(h, h->sc.n_bounces))) return rc;
         pbeg(h, st);
         kern::k_reset_queue<<<1, 1, 0, st>>>(h->ps.counters, 1);
-        kern::k_paths<<<g, kThreads, 0, st>>>(a, h->ms.geo);
+        if (paths < kCoopPaths) kern::k_paths_coop<<<grid_for(h, paths * 4), kThreads, 0, st>>>(a, h->ms.geo);
+        else kern::k_paths<<<g, kThreads, 0, st>>>(a, h->ms.geo);
         CK(cudaGetLastError());
         pend(h, HRT_STAGE_INTERSECT, st);
         h->launches += 2;

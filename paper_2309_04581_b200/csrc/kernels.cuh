@@ -443,6 +443,46 @@ __global__ void __launch_bounds__(256, HRT_PATHS_MINB) k_paths(Args a, PathGeo g
     if (blockIdx.x == 0 && threadIdx.x == 0) stat_add(s.stats, S_SEGMENTS, n);   // bounce-1 rays
 }
 
+// k_paths with 4 lanes per path (bvh::closest_q_coop), for chunks of few
+// paths where the longest per-path chain of traversals bounds the launch.
+__global__ void __launch_bounds__(256) k_paths_coop(Args a, PathGeo g) {
+    const int32_t n = a.ps.counters[C_Q0];
+    const int32_t* q = a.ps.queue[0];
+    const PathState& s = a.ps;
+    const uint32_t lane = threadIdx.x & 31u, gl = lane & 3u, gbase = lane - gl;
+    const uint32_t gmask = 0xFu << gbase;
+    const int32_t groups = (int32_t)(gridDim.x * blockDim.x / 4);
+    for (int32_t j = (int32_t)((blockIdx.x * blockDim.x + threadIdx.x) / 4); j < n; j += groups) {
+        const int32_t p = q[j];
+        d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+        const int32_t pix = s.pix[p], smp = s.smp[p];
+        for (int32_t b = 1; b <= a.sc.n_bounces; ++b) {
+            double t = INFINITY;
+            const int32_t f = bvh::closest_q_coop(a.sc.bvh, o, d, 0.0, INFINITY, t, gmask, gbase, gl);
+            const int64_t at = (int64_t)(b - 1) * g.cap + p;
+            if (gl == 0) {
+                g.t[at] = t;
+                g.face[at] = f;
+                if (b == 1) {
+                    s.t_hit[p] = t;
+                    s.face[p] = f;
+                }
+            }
+            if (f < 0 || b == a.sc.n_bounces) break;
+            d3 o2, d2;
+            spawn_ray(a, pix, smp, b, o, d, t, f, o2, d2);
+            o = o2;
+            d = d2;
+            if (gl == 0) {
+                const int64_t nx = at + g.cap;
+                g.ox[nx] = o.x; g.oy[nx] = o.y; g.oz[nx] = o.z;
+                g.dx[nx] = d.x; g.dy[nx] = d.y; g.dz[nx] = d.z;
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) stat_add(s.stats, S_SEGMENTS, n);   // bounce-1 rays
+}
+
 // Segment set-up of path p for the march of bounce `bounce`; false (n = 0)
 // when the ray has no segment inside the field box before its hit.
 HRT_DEV bool seg_one(const Args& a, const MarchState& m, int32_t p, int32_t bounce) {
