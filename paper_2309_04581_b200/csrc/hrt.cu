@@ -40,6 +40,10 @@ int fail(int code, const std::string& msg) {
 #endif
 constexpr int64_t kMaxPaths = int64_t(1) << HRT_MAX_PATHS_LOG2;   // paths per wavefront chunk
 constexpr int kThreads = 256;
+#ifndef HRT_STEP_THREADS
+#define HRT_STEP_THREADS 128
+#endif
+constexpr int kStepThreads = HRT_STEP_THREADS;     // k_step block size
 constexpr int kTimedLaunches = 1024;
 constexpr int kIoChunks = 4;                       // pieces of the e2e frame read-back
 #ifndef HRT_SHADOW_QUEUE
@@ -943,6 +947,8 @@ int shadow_trace(hrt_handle* h, const kern::Args& a, cudaStream_t st) {
 // k_gen -> k_field_ws -> k_comp until no path has midpoints left.
 int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream_t st) {
     const unsigned g = grid_for(h, n_paths);
+    const unsigned gs = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_paths + kStepThreads - 1) / kStepThreads,
+                                                                         (int64_t)h->sm_count * 16 * 256 / kStepThreads));
     int rc;
     if (!a.trace) {
         // Device-driven fused rounds, no host sync per round:
@@ -965,8 +971,8 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
             for (int k = 0; k < kRoundsPerCheck; ++k) {
                 pbeg(h, st);
                 kern::k_round_begin<<<1, 1, 0, st>>>(h->ps.counters, h->ps.stats, target, cap);
-                if (a.mixed) kern::k_step<true><<<g, kThreads, 0, st>>>(a, h->ms);
-                else kern::k_step<false><<<g, kThreads, 0, st>>>(a, h->ms);
+                if (a.mixed) kern::k_step<true><<<gs, kStepThreads, 0, st>>>(a, h->ms);
+                else kern::k_step<false><<<gs, kStepThreads, 0, st>>>(a, h->ms);
                 CK(cudaGetLastError());
                 pend(h, HRT_STAGE_COMPOSITE, st);
                 pbeg(h, st);

@@ -896,7 +896,10 @@ HRT_DEV void step_tail(const Args& a, const MarchState& m, int32_t first, int32_
 #define HRT_STEP_MINB 3
 #endif
 template <bool kMixed>
-__global__ void __launch_bounds__(256, HRT_STEP_MINB) k_step(Args a, MarchState m) {
+#ifndef HRT_STEP_THREADS
+#define HRT_STEP_THREADS 128
+#endif
+__global__ void __launch_bounds__(HRT_STEP_THREADS, HRT_STEP_MINB * 256 / HRT_STEP_THREADS) k_step(Args a, MarchState m) {
     const int32_t* ctr = a.ps.counters;
     const int32_t mcur = ctr[C_CUR], S = ctr[C_S], prev_nq = ctr[C_PSTRIDE], first = ctr[C_FIRST];
     const int32_t nq = ctr[C_MQ0 + mcur];
