@@ -1079,7 +1079,9 @@ int run_bounces(hrt_handle* h, kern::Args& a, int64_t paths, int mode, cudaStrea
         pbeg(h, st);
         kern::k_reset_queue<<<1, 1, 0, st>>>(h->ps.counters, 1);
         if (paths < kCoopPaths) kern::k_paths_coop<<<grid_for(h, paths * 4), kThreads, 0, st>>>(a, h->ms.geo);
-        else kern::k_paths<<<g, kThreads, 0, st>>>(a, h->ms.geo);
+        else kern::k_paths<<<(unsigned)std::min<int64_t>((paths + HRT_PATHS_THREADS - 1) / HRT_PATHS_THREADS,
+                                                         (int64_t)h->sm_count * 16 * 256 / HRT_PATHS_THREADS),
+                             HRT_PATHS_THREADS, 0, st>>>(a, h->ms.geo);
         CK(cudaGetLastError());
         pend(h, HRT_STAGE_INTERSECT, st);
         h->launches += 2;

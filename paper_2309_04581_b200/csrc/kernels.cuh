@@ -412,7 +412,10 @@ HRT_DEV bool shade_one(const Args& a, int32_t p, int32_t bounce, Acc& c) {
 #define HRT_PATHS_MINB 4
 #endif
 // 64 registers (4 blocks of 256 per SM): cfg3 (1.02 M triangles) -18 % vs 90 registers
-__global__ void __launch_bounds__(256, HRT_PATHS_MINB) k_paths(Args a, PathGeo g) {
+#ifndef HRT_PATHS_THREADS
+#define HRT_PATHS_THREADS 128
+#endif
+__global__ void __launch_bounds__(HRT_PATHS_THREADS, HRT_PATHS_MINB * 256 / HRT_PATHS_THREADS) k_paths(Args a, PathGeo g) {
     const int32_t n = a.ps.counters[C_Q0];
     const int32_t* q = a.ps.queue[0];
     const PathState& s = a.ps;
