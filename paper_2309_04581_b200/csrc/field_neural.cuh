@@ -51,10 +51,6 @@ HRT_DEV uint32_t corner_index(const NeuralLevel& lv, const LevelCoord& c, int co
     return (X ^ (Y * kHashY) ^ (Z * kHashZ)) & tmask;
 }
 
-#ifndef HRT_PAIR_GATHERS
-#define HRT_PAIR_GATHERS 0   // measured: coherent sample-major batches are issue-bound, pairing costs more than it saves
-#endif
-constexpr bool kPairGathers = HRT_PAIR_GATHERS;
 
 // acc (two packed fp32) = fma(w, v, acc) per lane of the pair: one FFMA2.
 // (a.x * b.x, a.y * b.y), each rounded as a scalar FMUL: one FMUL2.
@@ -89,17 +85,7 @@ HRT_DEV void gather_accumulate(const float* __restrict__ lvl_base, const uint32_
         const float2* base = reinterpret_cast<const float2*>(lvl_base);
         float2 v[8];
 #pragma unroll
-        for (int k = 0; k < 8; k += 2) {
-            if (kPairGathers && idx[k + 1] == (idx[k] ^ 1u)) {
-                const float4 q = __ldg(reinterpret_cast<const float4*>(base + (idx[k] & ~1u)));
-                const bool hi = idx[k] & 1u;
-                v[k] = hi ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
-                v[k + 1] = hi ? make_float2(q.x, q.y) : make_float2(q.z, q.w);
-            } else {
-                v[k] = __ldg(base + idx[k]);
-                v[k + 1] = __ldg(base + idx[k + 1]);
-            }
-        }
+        for (int k = 0; k < 8; ++k) v[k] = __ldg(base + idx[k]);
         float2 acc[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
 #pragma unroll
         for (int k = 0; k < 8; ++k) fma2(acc[k & 1], w[k], v[k]);
@@ -156,25 +142,10 @@ HRT_DEV void encode_level(const NeuralField& nf, const NeuralLevel& lv, float3 r
     }
 }
 
-// Two-phase form of encode_level for F = 2, used to keep two levels of
-// gathers in flight per thread: issue() computes the corner indices and
-// starts the 8 loads, finish() forms the weights and accumulates (same
-// arithmetic, same order as encode_level).
-#ifndef HRT_FINE_NOL1
-#define HRT_FINE_NOL1 0
-#endif
-#ifndef HRT_FINE_LEVEL_N
-#define HRT_FINE_LEVEL_N 512
-#endif
-constexpr bool kFineNoL1 = HRT_FINE_NOL1;
-constexpr int kFineLevelN = HRT_FINE_LEVEL_N;
-
-HRT_DEV float2 ld_na(const float2* p) {
-    float2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
-    return v;
-}
-
+// Two-phase form of a level for the field engine: level_issue() computes the
+// corner indices and starts the 8 loads, level_finish() forms the weights and
+// accumulates (same arithmetic, same order as encode_level), so two levels of
+// gathers can be in flight per thread.
 template <int F> struct FVec { using T = float2; };
 template <> struct FVec<4> { using T = float4; };
 
@@ -210,15 +181,7 @@ HRT_DEV void level_issue(const NeuralField& nf, const NeuralLevel& lv, float3 re
         const uint32_t xs[2] = {X & m, (X + 1u) & m};
         const uint32_t ys[2] = {hy & m, (hy + kHashY) & m};
         const uint32_t zs[2] = {(hz & m) | off, ((hz + kHashZ) & m) | off};
-        if (F == 2 && kFineNoL1 && lv.n >= kFineLevelN) {
-            // fine hashed levels have little L1 reuse: keep their fills out of L1
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const float2 t = ld_na(reinterpret_cast<const float2*>(nf.table) +
-                                       (xs[k & 1] ^ ys[(k >> 1) & 1] ^ zs[k >> 2]));
-                g.v[k] = *reinterpret_cast<const V*>(&t);
-            }
-        } else if (tex_level) {
+        if (tex_level) {
 #pragma unroll
             for (int k = 0; k < 8; ++k)
                 g.v[k] = tex1Dfetch<V>(nf.tex, (int)(xs[k & 1] ^ ys[(k >> 1) & 1] ^ zs[k >> 2]));
