@@ -1,16 +1,28 @@
 #!/usr/bin/env python
 """Benchmark: NeRF samples/s and Mrays/s per frame for the hybrid NeRF/mesh
-render path (BASELINE.json metric), on BASELINE config 1 (glass icosphere in
-an L16/T2^19 hash-grid NeRF, 800x800, 1 spp, 4 bounces, 100 cameras).
+render path (BASELINE.json metric) on BASELINE config 3 - the config the
+metric's "per frame at 1/2/4/8 B200" and the north star's "1->8-GPU Mrays/s
+scaling at 1080p" are quoted on:
 
-One step = one full 800x800 frame from camera (step mod 100), rendered by
-the sm_100a kernels through the C ABI with scene and network resident in
-HBM. With N GPUs (torchrun, one rank per GPU) the frame is split into 16x16
-pixel tiles dealt round-robin to ranks; every rank's accumulate kernel stores
-its pixels straight into rank 0's frame over peer memory (CUDA IPC, NVLink)
-- `--gather nccl` uses an NCCL all-gather instead
-(strong scaling: the frame is fixed). `--impl reference` times the CPU
-oracle port of the reference path (oracle/, numpy) on the host cores instead.
+  200 icospheres s4 (1,024,000 triangles; mirror / glass / diffuse) moving
+  rigidly inside the L16 F2 T2^19 hash-grid NeRF, 1920x1080, 8 spp, 4 bounces.
+
+One step = one frame of the 30-frame seeded motion (frame = step mod 30):
+`hrt_refit_rigid` (per-mesh transforms -> world faces -> BVH refit on the GPU,
+the reference's per-frame `sim.sync_to_renderer -> Scene.rebuild_bvh`,
+`sim.py:673-698`, `scene.py:475-479`), then the full frame
+(`render.py:372-380`), with scene and network resident in HBM. With N GPUs
+(one process per GPU) the frame is split into 16x16 pixel tiles dealt
+round-robin to ranks (`render.py:353-369`'s tile split); every
+rank's accumulate kernel stores its pixels straight into rank 0's frame over
+peer memory (CUDA IPC over NVLink) - `--gather nccl` uses an NCCL all-gather
+instead (strong scaling: the frame is fixed).
+
+`python bench.py --gpus N` without torchrun re-launches itself under
+`torch.distributed.run` with N ranks. `--config cfg1` times BASELINE config 1
+instead (cfg1 is also reported as an extra key of the default run).
+`--impl reference` times the CPU oracle port of the reference path (oracle/,
+numpy) on the host cores, on seeded crops of the same config.
 
 Prints one JSON line on rank 0.
 """
@@ -18,9 +30,10 @@ Prints one JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import glob
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,7 +45,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "NeRF samples/sec and Mrays/sec per frame at 1/2/4/8 B200 vs CPU ref"
 TILE = 16
-WORKLOAD = "cfg1: glass icosphere s5 (20480 tris, IOR 1.5) in L16 F2 T2^19 16->2048 hash-grid NeRF, 800x800, 1 spp, 4 bounces, 128^3 occupancy, 1024-sample cap, early-out 1e-4, 100 seeded cameras"
+WORKLOADS = {
+    "cfg3": "cfg3: 200 moving icospheres s4 (1,024,000 tris; mirror/glass/diffuse, seed 3) in the "
+            "L16 F2 T2^19 16->2048 hash-grid NeRF (seed 1), 1920x1080, 8 spp, 4 bounces, 128^3 "
+            "occupancy, 1024-sample cap, early-out 1e-4; each step = GPU rigid refit of the next of "
+            "30 seeded motion frames + the full frame",
+    "cfg1": "cfg1: glass icosphere s5 (20480 tris, IOR 1.5) in L16 F2 T2^19 16->2048 hash-grid NeRF, "
+            "800x800, 1 spp, 4 bounces, 128^3 occupancy, 1024-sample cap, early-out 1e-4, 100 seeded "
+            "cameras (step k = camera k mod 100)",
+}
+CFG3_FRAMES = 30
 
 
 def parse():
@@ -41,9 +63,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=["cfg3", "cfg1"], default="cfg3")
     ap.add_argument("--cpu-tiles", type=int, default=0,
-                    help="16x16 tiles per CPU-baseline sample (0 = 2 per worker process)")
+                    help="16x16 tiles per CPU sample (0 = scaled to the worker count)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg1 extra key")
     ap.add_argument("--gather", choices=["peer", "nccl"], default="peer",
                     help="frame assembly: peer-memory stores from the render (default) or NCCL all-gather")
     return ap.parse_args()
@@ -54,6 +78,34 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
     return rank, world, local
+
+
+def _free_port():
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args):
+    """`bench.py --gpus N` outside torchrun: re-launch under
+    torch.distributed.run with N ranks (one per GPU) and exit with its code.
+    Fails loudly when fewer than N GPUs are visible (HRT_DIST_BACKEND=gloo
+    lets N ranks share fewer GPUs to exercise the multi-rank flow)."""
+    if "WORLD_SIZE" in os.environ or args.gpus <= 1 or args.impl == "reference":
+        return
+    backend = os.environ.get("HRT_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        import torch
+        n = torch.cuda.device_count()
+        if n < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {n} "
+                  "(HRT_DIST_BACKEND=gloo shares GPUs for a functional multi-rank run)",
+                  file=sys.stderr, flush=True)
+            sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd, env=dict(os.environ)))
 
 
 # ------------------------------------------------------------ clocks ----
@@ -122,59 +174,86 @@ def peaks():
         return 6650.0, 1400.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes and L2->L1 requests / sectors per sample of the
-    field engine from the committed ncu capture (profiles/r01e_field_traffic.json,
-    made by tools/field_traffic.py)."""
-    path = os.path.join(ROOT, "profiles", "r01e_field_traffic.json")
+def ncu_traffic(config):
+    """Field-engine L2 traffic per sample from the newest committed ncu
+    capture of this config (profiles/*_field_traffic_<config>.json, made by
+    tools/field_traffic.py from an ncu run over every k_field_ws launch of
+    one frame; the file names the commit it was captured at)."""
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*field_traffic_{config}.json")))
+    if not paths:
+        return None, None
     try:
-        with open(path) as f:
-            return json.load(f)
+        with open(paths[-1]) as f:
+            return json.load(f), os.path.relpath(paths[-1], ROOT)
     except (OSError, ValueError):
-        return None
+        return None, None
 
 
 # --------------------------------------------------- CPU baseline (oracle) -
 
-_CPU_SCENE = None
+_CPU = {}
 
 
-def _cpu_scene():
-    """Oracle scene for cfg1, built once in the parent (scene load, BVH and
-    occupancy build are outside the timed sample, as for the GPU arm) and
+def _cpu_scene(config):
+    """Oracle scene of the config, built once in the parent (scene build,
+    BVH and occupancy are outside the timed sample, as for the GPU arm) and
     inherited by the forked workers."""
-    global _CPU_SCENE
-    if _CPU_SCENE is None:
+    if config not in _CPU:
         from oracle import tracer
-        from oracle.field import occupancy_bits
         from paper_2309_04581_b200 import configs
-        from paper_2309_04581_b200.pack import pack_scene
-        _CPU_SCENE = tracer.OracleScene(pack_scene(configs.cfg1()))
-        occupancy_bits(_CPU_SCENE.field)
-    return _CPU_SCENE
+        from paper_2309_04581_b200.pack import pack_camera, pack_scene
+        scene = configs.cfg3() if config == "cfg3" else configs.cfg1()
+        _CPU[config] = (tracer.OracleScene(pack_scene(scene)), pack_camera(scene.camera))
+    return _CPU[config]
+
+
+def _occ_rows(args):
+    config, lo, hi = args
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+    from oracle.field import neural_encode, neural_mlp
+    fp = _cpu_scene(config)[0].field
+    g = int(fp["occ_res"])
+    c = np.arange(lo, hi)
+    ijk = np.stack([c % g, (c // g) % g, c // (g * g)], axis=1).astype(np.float64)
+    pf = fp["bbox_lo"] + (ijk + 0.5) * ((fp["bbox_hi"] - fp["bbox_lo"]) / g)
+    sigma, _ = neural_mlp(fp, neural_encode(fp, pf), None, density_only=True)
+    return lo, sigma > fp["occ_threshold"]
+
+
+def _cpu_occupancy(config, pool):
+    """The oracle's occupancy bitfield (oracle.field.build_occupancy, cell i =
+    x + G*(y + G*z)), computed in slices over the worker pool."""
+    import numpy as np
+    fp = _cpu_scene(config)[0].field
+    if "_occ_cache" in fp or fp.get("occ_bits") is not None:
+        return
+    g = int(fp["occ_res"])
+    n = g ** 3
+    step = 1 << 14
+    occ = np.zeros(n, bool)
+    for lo, m in pool.map(_occ_rows, [(config, a, min(n, a + step)) for a in range(0, n, step)]):
+        occ[lo:lo + len(m)] = m
+    words = np.zeros((n + 31) // 32, np.uint32)
+    idx = np.nonzero(occ)[0]
+    np.bitwise_or.at(words, idx >> 5, (np.uint32(1) << (idx & 31).astype(np.uint32)))
+    fp["_occ_cache"] = words
 
 
 def _cpu_tile(args):
-    cam_index, pixels = args
+    config, frame_cam, pixels, spp = args
     from threadpoolctl import threadpool_limits
     threadpool_limits(1)                 # one BLAS thread per worker process
     from oracle import tracer
-    from paper_2309_04581_b200 import configs
-    from paper_2309_04581_b200.pack import pack_camera
-    cam = pack_camera(configs.cfg1_cameras()[cam_index])
+    sc, cam = _cpu_scene(config)
+    if config == "cfg1":
+        from paper_2309_04581_b200 import configs
+        from paper_2309_04581_b200.pack import pack_camera
+        cam = pack_camera(configs.cfg1_cameras()[frame_cam])
     st = {}
-    tracer.render(_cpu_scene(), cam, 1, 0, pixels=pixels, stats=st)
+    tracer.render(sc, cam, spp, 0, pixels=pixels, stats=st)
     return st["nerf_samples"], st["paths"]
-
-
-def cpu_pool(workers):
-    """One forked worker per core, created once (scene inherited, imports
-    warmed by a tiny job) so timed samples measure tracing, not start-up."""
-    import multiprocessing as mp
-    _cpu_scene()
-    pool = mp.get_context("fork").Pool(workers)
-    pool.map(_warm, range(workers))
-    return pool
 
 
 def _warm(_):
@@ -184,30 +263,42 @@ def _warm(_):
     return 0
 
 
-def cpu_sample(n_tiles, workers, cam_index=0, seed=0, pool=None):
+def cpu_pool(config, workers):
+    """One forked worker per core, created once (scene inherited, imports
+    warmed by a tiny job) so timed samples measure tracing, not start-up;
+    the oracle occupancy grid is built on the pool before it is forked
+    again for the tiles."""
+    import multiprocessing as mp
+    _cpu_scene(config)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers) as p:
+        _cpu_occupancy(config, p)
+    pool = ctx.Pool(workers)              # forked after the occupancy cache exists
+    pool.map(_warm, range(workers))
+    return pool
+
+
+def _frame_shape(config):
+    return ((1920, 1080), 8) if config == "cfg3" else ((800, 800), 1)
+
+
+def cpu_sample(config, n_tiles, pool, cam_index=0, seed=0):
     """Oracle (numpy port of the reference path) on `n_tiles` seeded 16x16
-    tiles of the cfg1 frame, one process per core."""
+    tiles of the config's frame, one process per core."""
     import numpy as np
+    (w, h), spp = _frame_shape(config)
     rng = np.random.default_rng(seed)
-    all_t = (800 // TILE) * (800 // TILE)
-    chosen = rng.choice(all_t, n_tiles, replace=False)
+    tx = w // TILE
+    chosen = rng.choice(tx * (h // TILE), n_tiles, replace=False)
     jobs = []
     for t in chosen:
-        x0, y0 = (t % (800 // TILE)) * TILE, (t // (800 // TILE)) * TILE
+        x0, y0 = (t % tx) * TILE, (t // tx) * TILE
         ys, xs = np.meshgrid(np.arange(y0, y0 + TILE), np.arange(x0, x0 + TILE), indexing="ij")
-        jobs.append((cam_index, (ys * 800 + xs).reshape(-1)))
-    own = pool is None
-    if own:
-        pool = cpu_pool(workers)
+        jobs.append((config, cam_index, (ys * w + xs).reshape(-1), spp))
     t0 = time.perf_counter()
     res = pool.map(_cpu_tile, jobs, chunksize=1)
     dt = time.perf_counter() - t0
-    if own:
-        pool.close()
-        pool.join()
-    samples = sum(r[0] for r in res)
-    paths = sum(r[1] for r in res)
-    return samples, paths, dt
+    return sum(r[0] for r in res), sum(r[1] for r in res), dt
 
 
 def cpu_workers():
@@ -217,18 +308,67 @@ def cpu_workers():
         return os.cpu_count() or 1
 
 
-def cpu_baseline_block(n_tiles=0):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def shipped_block(workers):
+    """The unmodified reference (baseline/_ref) with a dense-grid stand-in on
+    seeded cfg3 tiles, one process per core (oracle/shipped.py)."""
+    import multiprocessing as mp
+
+    import numpy as np
+
+    from oracle import shipped
+    try:
+        where = shipped.import_reference()
+    except Exception as e:          # noqa: BLE001 - context only
+        return {"unavailable": f"reference import failed: {e}"}
+    if where is None:
+        return {"unavailable": "hybridrt not installed in baseline/_ref"}
+    t0 = time.perf_counter()
+    shipped.scene()                  # reference Bvh build over 1.02 M triangles (outside the timing)
+    build_s = time.perf_counter() - t0
+    tiles = list(np.random.default_rng(7).choice((1920 // TILE) * (1080 // TILE), 2 * workers,
+                                                  replace=False))
+    with mp.get_context("fork").Pool(workers) as pool:
+        pool.map(shipped.tile_job, tiles[:workers])          # warm
+        t0 = time.perf_counter()
+        res = pool.map(shipped.tile_job, tiles, chunksize=1)
+        dt = time.perf_counter() - t0
+    samples = sum(r[0] for r in res)
+    paths = sum(r[1] for r in res)
+    return {"value": samples / dt, "unit": "field samples/s", "mrays_per_s": paths / dt / 1e6,
+            "cores": workers, "kind": "reference",
+            "sample": f"{len(tiles)} seeded 16x16 x 8 spp tiles of the cfg3 frame-0 geometry through the "
+                      f"UNMODIFIED reference tracer (hybridrt from {os.path.relpath(where, ROOT) if where.startswith(ROOT) else where}: "
+                      "_sample_jitter -> Camera.primary_rays -> _trace_batch_hybrid) with a dense 64^3 "
+                      f"RadianceGrid fog in place of the NeRF it does not implement; one process per core, "
+                      f"{dt:.1f} s wall ({paths} paths, {samples} field samples; reference Bvh build "
+                      f"{build_s:.1f} s not timed)"}
+
+
+def cpu_baseline_block(config, n_tiles=0):
     workers = cpu_workers()
-    n_tiles = n_tiles or max(16, 8 * workers)
-    pool = cpu_pool(workers)             # forked + warmed before the timed sample
-    samples, paths, dt = cpu_sample(n_tiles, workers, pool=pool)
+    (w, h), spp = _frame_shape(config)
+    n_tiles = n_tiles or (2 * workers if config == "cfg3" else max(16, 8 * workers))
+    pool = cpu_pool(config, workers)
+    samples, paths, dt = cpu_sample(config, n_tiles, pool)
     pool.close()
     pool.join()
     return {"value": samples / dt, "unit": "samples/s", "cores": workers, "kind": "port",
-            "mrays_per_s": paths / dt / 1e6,
-            "sample": f"{n_tiles} seeded 16x16 tiles ({paths} paths, {samples} NeRF samples) of the "
-                      f"cfg1 camera-0 frame, oracle/ numpy port of the reference path, one process "
-                      f"per core, {dt:.1f} s wall"}
+            "cpu": cpu_model(), "mrays_per_s": paths / dt / 1e6,
+            "sample": f"{n_tiles} seeded 16x16 x {spp} spp tiles ({paths} paths, {samples} NeRF samples) "
+                      f"of the {config} frame-0 {w}x{h} frame, oracle/ numpy port of the reference "
+                      f"render loop + neural field, one process per core, {dt:.1f} s wall",
+            "reference_as_shipped": shipped_block(workers) if config == "cfg3" else None}
 
 
 # ------------------------------------------------------------ arms ------
@@ -237,27 +377,31 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     workers = cpu_workers()
-    n_tiles = args.cpu_tiles or max(8, 4 * workers)
-    pool = cpu_pool(workers)
+    (w, h), spp = _frame_shape(args.config)
+    n_tiles = args.cpu_tiles or (workers if args.config == "cfg3" else max(8, 4 * workers))
+    pool = cpu_pool(args.config, workers)
     for _ in range(max(0, min(args.warmup, 1))):
-        cpu_sample(max(1, workers), workers, pool=pool)
+        cpu_sample(args.config, max(1, workers), pool)
     tot_s = tot_p = tot_t = 0.0
     for k in range(args.steps):
-        s, p, dt = cpu_sample(n_tiles, workers, cam_index=k % 100, seed=k, pool=pool)
+        s, p, dt = cpu_sample(args.config, n_tiles, pool, cam_index=k % 100, seed=k)
         tot_s, tot_p, tot_t = tot_s + s, tot_p + p, tot_t + dt
     pool.close()
     pool.join()
     value = tot_s / tot_t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": max(world, args.gpus), "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "mrays_per_s": tot_p / tot_t / 1e6,
-        "config": {"workload": WORKLOAD + f"; CPU sample per step = {n_tiles} seeded 16x16 tiles"},
+        "config": {"workload": WORKLOADS[args.config] + f"; CPU sample per step = {n_tiles} seeded "
+                                                        f"16x16 x {spp} spp tiles of frame 0",
+                   "frame": [w, h]},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": workers, "kind": "port",
-                         "sample": f"{n_tiles} seeded 16x16 tiles per step x {args.steps} steps, "
-                                   f"oracle/ numpy port of the reference render loop + neural "
+                         "cpu": cpu_model(),
+                         "sample": f"{n_tiles} seeded 16x16 x {spp} spp tiles per step x {args.steps} "
+                                   f"steps, oracle/ numpy port of the reference render loop + neural "
                                    f"field, one process per core (pool forked and warmed once)"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -290,15 +434,97 @@ def open_peer_frame(w, h, rank, world):
     return peer
 
 
+class Workload:
+    """The timed scene: renderer + per-step inputs (camera, spp, motion)."""
+
+    def __init__(self, config, dev):
+        import numpy as np
+
+        from paper_2309_04581_b200 import assets, configs
+        from paper_2309_04581_b200.renderer import Renderer
+        self.config = config
+        if config == "cfg3":
+            self.scene = configs.cfg3()
+            self.r = Renderer(self.scene)
+            base_v, base_f = assets.icosphere(1.0, 4)
+            n = len(self.scene.meshes)
+            self.r.set_rigid_base([base_v] * n, [base_f] * n)
+            # the 30 frames' transforms in page-locked host memory (e2e H2D source)
+            self.xf = [Renderer.pinned((n, 3, 4), np.float64) for _ in range(CFG3_FRAMES)]
+            for f in range(CFG3_FRAMES):
+                self.xf[f][:] = configs.cfg3_transforms(f)
+            self.cams = [self.scene.camera]
+            self.spp = self.scene.render.spp
+        else:
+            self.scene = configs.cfg1()
+            self.r = Renderer(self.scene)
+            self.xf = None
+            self.cams = configs.cfg1_cameras()
+            self.spp = 1
+        self.field = self.scene.field
+        self.w, self.h = self.cams[0].resolution
+
+    def prepare(self, k):
+        """Per-frame scene update (cfg3: refit to motion frame k mod 30)."""
+        if self.xf is not None:
+            self.r.refit_rigid(self.xf[k % CFG3_FRAMES])
+
+    def camera(self, k):
+        return self.cams[k % len(self.cams)]
+
+    def h2d_update_bytes(self):
+        return 0 if self.xf is None else int(self.xf[0].nbytes)
+
+
+def time_frames(wl, steps, warmup, pix, peer, out, gather, flush, stream, k0=0):
+    """Device time of `steps` frames (after `warmup`): per step the scene
+    update + the render of this rank's tiles (+ the NCCL gather when there is
+    no peer frame), CUDA events on the launching stream."""
+    import torch
+    n_local = int(pix.numel())
+    res = []
+
+    def step(k, timed):
+        if timed:
+            flush.fill_(float(k))          # evict L2 between timed steps (outside the events)
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+        wl.prepare(k)
+        if timed:
+            e1.record(stream)
+        if peer is not None:               # pixels stored into rank 0's frame (peer memory)
+            wl.r.render_pixels(wl.camera(k), wl.spp, 0, pixels=pix, frame_ptr=peer.ptr)
+            st = dict(wl.r.last_stats)
+            if timed:
+                e2.record(stream)
+            peer.done()                    # stream sync + barrier: rank 0's frame complete
+        else:
+            wl.r.render_pixels(wl.camera(k), wl.spp, 0, pixels=pix, out=out[:n_local])
+            st = dict(wl.r.last_stats)
+            gather.gather()                # frame assembled on rank 0 (NCCL all-gather)
+            if timed:
+                e2.record(stream)
+        if timed:
+            e2.synchronize()
+            st["step_ms"] = e0.elapsed_time(e2)
+            st["refit_ms"] = e0.elapsed_time(e1)
+        return st
+
+    for k in range(warmup):
+        step(k0 + k, False)
+    return [step(k0 + warmup + k, True) for k in range(steps)]
+
+
 def run_ours(args, rank, world, local):
     import numpy as np
     import torch
     import torch.distributed as dist
 
-    from paper_2309_04581_b200 import configs
-    from paper_2309_04581_b200.renderer import Renderer
-    from paper_2309_04581_b200.tiles import FrameGather, PeerFrame, tile_pixels
+    from paper_2309_04581_b200.renderer import Renderer, finalize_device
+    from paper_2309_04581_b200.tiles import FrameGather, tile_pixels
 
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     # one process per GPU; HRT_DIST_BACKEND=gloo lets several ranks share one GPU to test the
     # multi-rank flow where only one device exists (timings then mean nothing)
     dev_index = local % max(1, torch.cuda.device_count())
@@ -307,14 +533,13 @@ def run_ours(args, rank, world, local):
     backend = os.environ.get("HRT_DIST_BACKEND", "nccl")
     if world > 1:
         if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")          # NVLink / NVLS transport choice in the log
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    scene = configs.cfg1()
-    cams = configs.cfg1_cameras()
-    field = scene.field
-    r = Renderer(scene)
-    w, h = cams[0].resolution
+    wl = Workload(args.config, dev)
+    w, h = wl.w, wl.h
     pix_host = tile_pixels(w, h, rank, world)
     pix = torch.as_tensor(pix_host, device=dev)
     n_local = len(pix_host)
@@ -324,96 +549,116 @@ def run_ours(args, rank, world, local):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
-    def step(k, timed):
-        cam = cams[k % len(cams)]
-        if timed:
-            flush.fill_(float(k))          # evict L2 between timed steps (outside the events)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        if peer is not None:               # pixels stored into rank 0's frame (peer memory)
-            r.render_pixels(cam, 1, 0, pixels=pix, frame_ptr=peer.ptr)
-            st = dict(r.last_stats)
-            peer.done()
-        else:
-            r.render_pixels(cam, 1, 0, pixels=pix, out=out[:n_local])
-            st = dict(r.last_stats)
-            gather.gather()                # frame assembled on rank 0 (NCCL all-gather)
-        if timed:
-            e1.record(stream)
-            e1.synchronize()
-            st["step_ms"] = e0.elapsed_time(e1)
-        return st
-
-    for k in range(args.warmup):
-        step(k, False)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(dev_index)
     clocks.start()
     t_wall = time.perf_counter()
-    steps = [step(args.warmup + k, True) for k in range(args.steps)]
+    steps = time_frames(wl, args.steps, args.warmup, pix, peer, out, gather, flush, stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t_wall = time.perf_counter() - t_wall
     clk = clocks.stop()
 
-    dev_ms = sum(s["step_ms"] for s in steps)
-    samples = sum(s["nerf_samples"] for s in steps)
-    paths = sum(s["paths"] for s in steps)
-    march_ms = sum(s["field_ms"] for s in steps)
-    march_n = sum(s["field_launches"] for s in steps)
-    evaluated = sum(s["evaluated"] for s in steps)
-    launches = sum(s["launches"] for s in steps)
-    t = torch.tensor([dev_ms, samples, paths, march_ms, march_n, launches], dtype=torch.float64,
-                     device=dev)
-    tmax = t.clone()
+    # frame time = the slowest rank's step time, per step (max over ranks)
+    per_step = torch.tensor([s["step_ms"] for s in steps], dtype=torch.float64, device=dev)
+    sums = torch.tensor([sum(s[k] for s in steps) for k in
+                         ("nerf_samples", "paths", "field_ms", "field_launches", "launches", "evaluated",
+                          "refit_ms")], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    max_ms = float(tmax[0])
-    tot_samples, tot_paths = float(t[1]), float(t[2])
+        dist.all_reduce(per_step, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+    max_ms = float(per_step.sum())
+    tot_samples, tot_paths = float(sums[0]), float(sums[1])
     value = tot_samples / (max_ms * 1e-3)
+    rank0 = {k: sum(s[k] for s in steps) for k in ("field_ms", "field_launches", "evaluated", "launches",
+                                                   "refit_ms")}
 
-    # ---- e2e: the public host-buffer C-ABI call, H2D + D2H inside --------
-    host_pix = Renderer.pinned((n_local,), np.int32)             # pinned host buffers (contract)
-    host_pix[:] = pix_host
-    host_out = Renderer.pinned((n_local, 3), np.float64)
-    r.render_host(cams[0], 1, 0, pixels=host_pix, out=host_out)          # warm
-    e2e_ms = []
-    e2e_samples = 0
+    # ---- e2e: the public API from host inputs to the host result --------
+    # per step: H2D of the frame's transforms (pinned) -> hrt_refit_rigid, H2D of the rank's
+    # pixel ids (pinned), render into rank 0's frame (peer stores or NCCL gather), then rank 0
+    # encodes the frame (hrt_finalize, PFM = the CLI's output) and reads it back to host.
+    pix_pinned = torch.from_numpy(Renderer.pinned((n_local,), np.int32))
+    pix_pinned.numpy()[:] = pix_host
+    pix_e2e = torch.empty_like(pix)
+    pfm_host = None
+    e2e_ms, e2e_samples, d2h = [], 0, 0
+
+    def e2e_step(k):
+        nonlocal pfm_host, d2h
+        wl.prepare(k)                                    # H2D transforms inside (cfg3)
+        pix_e2e.copy_(pix_pinned, non_blocking=True)
+        if peer is not None:
+            wl.r.render_pixels(wl.camera(k), wl.spp, 0, pixels=pix_e2e, frame_ptr=peer.ptr)
+            st = dict(wl.r.last_stats)
+            peer.done()
+            frame = peer.frame() if rank == 0 else None
+        else:
+            wl.r.render_pixels(wl.camera(k), wl.spp, 0, pixels=pix_e2e, out=out[:n_local])
+            st = dict(wl.r.last_stats)
+            frame = gather.gather()
+        if rank == 0:
+            pfm = finalize_device(frame, w, h, hdr_output=True)
+            if pfm_host is None:
+                pfm_host = torch.empty(pfm.shape, dtype=torch.uint8, pin_memory=True)
+            pfm_host.copy_(pfm)                          # D2H of the encoded frame
+            d2h = int(pfm.numel())
+        return st
+
+    e2e_step(0)                                          # warm (finalize buffers)
     for k in range(args.steps):
         flush.fill_(float(k))
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        r.render_host(cams[(args.warmup + k) % len(cams)], 1, 0, pixels=host_pix, out=host_out)
+        st = e2e_step(args.warmup + k)
+        torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        e2e_samples += r.last_stats["nerf_samples"]
-    e2 = torch.tensor([sum(e2e_ms), e2e_samples], dtype=torch.float64, device=dev)
-    e2max = e2.clone()
+        e2e_samples += st["nerf_samples"]
+    e2 = torch.tensor(e2e_ms + [e2e_samples], dtype=torch.float64, device=dev)
     if world > 1:
+        mx = e2.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(e2, op=dist.ReduceOp.SUM)
-        dist.all_reduce(e2max, op=dist.ReduceOp.MAX)
-    e2e_value = float(e2[1]) / (float(e2max[0]) * 1e-3)
+        e2[:-1] = mx[:-1]
+    e2e_value = float(e2[-1]) / (float(e2[:-1].sum()) * 1e-3)
 
-    # ---- untimed extras: per-stage breakdown of one frame, gather roofline probe
-    r.set_profile(True)
-    r.render_pixels(cams[0], 1, 0, pixels=pix, out=out[:n_local])
-    stages = {k: round(v, 3) for k, v in r.last_stats["stage_ms"].items()}
-    stage_frame_ms = r.last_stats["ms"]
-    r.set_profile(False)
-    gather_gbs = r.gather_peak(2)
+    # ---- untimed extras: per-stage breakdown of one frame, L2 / gather peaks, cfg1
+    wl.r.set_profile(True)
+    wl.prepare(args.warmup)
+    wl.r.render_pixels(wl.camera(args.warmup), wl.spp, 0, pixels=pix, out=out[:n_local])
+    stages = {k: round(v, 3) for k, v in wl.r.last_stats["stage_ms"].items()}
+    stage_frame_ms = wl.r.last_stats["ms"]
+    wl.r.set_profile(False)
+    gather_gbs = wl.r.gather_peak(2)
+    l2 = wl.r.l2_peak()
+
+    extra = None
+    if rank == 0 and world == 1 and args.config == "cfg3" and not args.no_extra:
+        wl.r.close()
+        w1 = Workload("cfg1", dev)
+        p1 = torch.as_tensor(tile_pixels(w1.w, w1.h, 0, 1), device=dev)
+        o1 = torch.empty((p1.numel(), 3), dtype=torch.float64, device=dev)
+        s1 = time_frames(w1, 10, 3, p1, None, o1, _NoGather(), flush, stream)
+        ms1 = sum(s["step_ms"] for s in s1)
+        extra = {"workload": WORKLOADS["cfg1"], "steps": 10, "ms_per_step": ms1 / 10,
+                 "value": sum(s["nerf_samples"] for s in s1) / (ms1 * 1e-3), "unit": "samples/s",
+                 "mrays_per_s": sum(s["paths"] for s in s1) / (ms1 * 1e-3) / 1e6}
+        w1.r.close()
 
     if rank == 0:
         hbm, tflops, peak_src = peaks()
+        field = wl.field
         enc_bytes = 8 * field.n_levels * field.n_features * 4            # 1024 B / sample
         mlp_flop = 2 * (field.enc_dim * 64 + 64 * 16 + 31 * 64 + 64 * 64 + 64 * 3)
-        march_samples = evaluated                                          # rank-0 field-engine evaluations
-        achieved = march_samples * enc_bytes / (march_ms * 1e-3) / 1e9
-        traffic = ncu_traffic() or {}
+        march_ms, march_samples = rank0["field_ms"], rank0["evaluated"]   # rank-0 field engine
         field_sps = march_samples / (march_ms * 1e-3)                      # samples/s inside the engine
-        sec_per_sample = traffic.get("l2_sectors_per_sample")
+        achieved = field_sps * enc_bytes / 1e9
+        traffic, traffic_src = ncu_traffic(args.config)
+        traffic = traffic or {}
         req_per_sample = traffic.get("l2_requests_per_sample")
         peak_requests = gather_gbs * 1e9 / 8.0                             # one request per random 8-B gather
         line = {
@@ -424,57 +669,81 @@ def run_ours(args, rank, world, local):
             "data": "synthetic (seeded random-init NeRF + procedural meshes, SURVEY Appendix B)",
             "mrays_per_s": tot_paths / (max_ms * 1e-3) / 1e6,
             "nerf_samples_per_frame": tot_samples / args.steps,
-            "config": {"workload": WORKLOAD, "frame": [w, h], "tile": TILE,
+            "config": {"workload": WORKLOADS[args.config], "frame": [w, h], "spp": wl.spp, "tile": TILE,
                        "parallelism": f"16x16 pixel tiles round-robin over {world} GPU(s); " + (
                            "each rank's k_accumulate stores its pixels into rank 0's frame over peer memory "
                            "(CUDA IPC / NVLink), then a barrier" if peer is not None
                            else "NCCL all-gather to rank 0"),
+                       "step": "refit (hrt_refit_rigid) + frame; frame time = max over ranks per step"
+                               if args.config == "cfg3" else "frame; max over ranks per step",
                        "l2": "256 MB buffer written before every timed step, outside the CUDA-event window",
-                       "wall_s_timed_region": t_wall},
-            "gpu_launches": int(launches),
+                       "wall_s_timed_region": t_wall,
+                       "refit_ms_per_step": rank0["refit_ms"] / args.steps},
+            "gpu_launches": int(rank0["launches"]),
             "roofline": {
-                "bound": "hbm", "kernel": "fws::k_field_ws<32,2> (warp-specialized hash encode + 5-layer tcgen05 MLP, TMEM operands)",
-                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "bound": "l2", "kernel": "fws::k_field_ws<32,2> (warp-specialized hash encode + 5-layer "
+                                         "tcgen05 MLP, TMEM operands)",
+                "achieved": achieved, "peak": l2["read_gbs"], "unit": "GB/s",
+                "frac": achieved / l2["read_gbs"],
                 "traffic": traffic.get("dram_bytes_per_launch"),
-                "bytes_per_sample": enc_bytes, "launches": int(march_n),
-                "avg_launch_ms": march_ms / max(1, march_n),
-                "peak_source": peak_src + " hbm_gbs (burst copy); the 46.5 MiB table is L2-resident, "
-                               "so frac > 1 vs HBM: the real limiter is roofline_gather",
+                "l2_bytes_per_launch": traffic.get("l2_bytes_per_launch"),
+                "bytes_per_sample": enc_bytes, "launches": int(rank0["field_launches"]),
+                "avg_launch_ms": march_ms / max(1, rank0["field_launches"]),
+                "peak_source": "hrt_l2_peak (live, this run): coalesced 16-B reads of an L2-resident "
+                               f"{l2['bytes'] / 2**20:.1f} MiB buffer (the hash table's size) by every SM; "
+                               "achieved = algorithmic encode bytes (8 corners x L x F x 4 B) x field-engine "
+                               "samples/s; traffic = ncu dram bytes per field-engine launch (" +
+                               (traffic_src or "no capture") + ")",
+                "hbm": {"peak": hbm, "frac": achieved / hbm, "source": peak_src + " hbm_gbs (burst copy); "
+                        "the 46.5 MiB table is L2-resident, so HBM is not the bound"},
             },
             "roofline_gather": {
                 "bound": "L1 miss requests to L2 (random gathers, ~1 request/clk/SM)",
                 "achieved": field_sps * req_per_sample if req_per_sample else None,
                 "peak": peak_requests, "unit": "requests/s",
                 "frac": field_sps * req_per_sample / peak_requests if req_per_sample else None,
-                "requests_per_sample": req_per_sample, "sectors_per_sample": sec_per_sample,
+                "requests_per_sample": req_per_sample,
+                "sectors_per_sample": traffic.get("l2_sectors_per_sample"),
+                "random_sector_gbs": l2["gather_sector_gbs"],
                 "peak_source": "hrt_gather_peak (live, this run): independent random 8-B gathers over the "
                                f"same table, {gather_gbs:.0f} GB/s useful = 1 request each; requests/sample from "
-                               "profiles/r01e_field_traffic.json (ncu lts__t_requests_srcunit_tex_op_read over a "
-                               "frame's field-engine launches)",
+                               f"{traffic_src} (ncu lts__t_requests_srcunit_tex_op_read over every field-engine "
+                               f"launch of one frame, commit {traffic.get('commit')})",
             },
-            "roofline_mlp": {"bound": "tensor", "achieved": march_samples * mlp_flop / (march_ms * 1e-3) / 1e12,
+            "roofline_mlp": {"bound": "tensor", "achieved": field_sps * mlp_flop / 1e12,
                              "peak": tflops, "unit": "TFLOP/s",
-                             "frac": march_samples * mlp_flop / (march_ms * 1e-3) / 1e12 / tflops,
+                             "frac": field_sps * mlp_flop / 1e12 / tflops,
                              "flop_per_sample": mlp_flop, "peak_source": peak_src + " bf16_tflops_sustained"},
             "e2e": {"value": e2e_value, "unit": "samples/s",
-                    "h2d_bytes_per_step": int(4 * n_local), "d2h_bytes_per_step": int(24 * n_local),
-                    "path": "hrt_render_host (pinned host pixel list in, pinned host float64 frame out, direct DMA both ways), wall clock"},
+                    "h2d_bytes_per_step": int(wl.h2d_update_bytes() + 4 * n_local),
+                    "d2h_bytes_per_step": d2h,
+                    "path": "per step: transforms (pinned) -> hrt_refit_rigid, pixel ids (pinned) H2D, "
+                            "hrt_render of the rank's tiles into rank 0's frame, barrier, rank 0 "
+                            "hrt_finalize (PFM) + D2H to pinned host; wall clock, max over ranks"},
             "clocks": clk,
             "stages_ms": {"frame_ms": stage_frame_ms, **stages,
-                          "note": "one untimed camera-0 frame with hrt_set_profile (event pair per launch)"},
+                          "note": "one untimed frame with hrt_set_profile (event pair per launch)"},
         }
+        if extra:
+            line["cfg1"] = extra
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline_block(args.cpu_tiles)
+            line["cpu_baseline"] = cpu_baseline_block(args.config, args.cpu_tiles)
         print(json.dumps(line), flush=True)
     if peer is not None:
         peer.close()
-    r.close()
+    wl.r.close()
     if world > 1:
         dist.destroy_process_group()
 
 
+class _NoGather:
+    def gather(self):
+        return None
+
+
 def main():
     args = parse()
+    maybe_spawn(args)
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)

@@ -133,6 +133,8 @@ typedef struct {
     int64_t rounds;               /* march rounds (generate -> field -> composite) */
     float stage_ms[8];            /* per-stage device time (HRT_STAGE_*), only after hrt_set_profile(h, 1) */
     int64_t batch_rows;           /* field-engine rows launched (samples + holes) */
+    int64_t shadow_traced;        /* shadow rays traced (>= shadow_rays: batch rows past an
+                                     early-out / cap are traced, then discarded by the composite) */
 } hrt_stats;
 
 /* Pipeline stages timed by hrt_set_profile (CUDA events around every launch). */
@@ -243,6 +245,18 @@ int hrt_ipc_close(void* ptr);
  * independent random 8-byte gathers over this scene's hash table (F = 2),
  * through the LSU path (mode 0), the TEX path (1) or both at once (2). */
 int hrt_gather_peak(hrt_handle* h, int32_t mode, double* gbs);
+
+/* Move the field (reference: a dynamic field object's world_from_field is
+ * reassigned between frames, sim.py:673-698, without a BVH rebuild):
+ * identity != 0, or the new row-major 4x4 field_from_world (rigid). The
+ * occupancy grid and the network live in the field frame and are kept. */
+int hrt_set_field_transform(hrt_handle* h, int32_t identity, const double* field_from_world);
+
+/* L2 roofline probe (bench.py "roofline"): GB/s of coalesced 16-B reads of
+ * this scene's hash table while it is L2-resident (all SMs, 8 passes), and
+ * GB/s of random whole 32-B sector gathers over it (lane pairs, L1
+ * bypassed); *bytes = the table's size. Device-synchronous, default stream. */
+int hrt_l2_peak(hrt_handle* h, double* read_gbs, double* sector_gbs, int64_t* bytes);
 
 /* New world-space face geometry (same topology; host pointers). */
 int hrt_refit(hrt_handle* h, const double* v0, const double* e1, const double* e2,

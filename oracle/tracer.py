@@ -168,6 +168,7 @@ def march(sc, ids, o, d, s_end, bounce, pix, smp, seed, st, trace=None):
         if shadows:
             need = (a > 0.0) & (rad.max(axis=1) > 0.0)
             if need.any():
+                st["nshadow"] = st.get("nshadow", 0) + int(need.sum())
                 m = np.ones(len(a))
                 m[need] = shadow_mask(sc, p[need], seed, pix[sel[need]], smp[sel[need]],
                                       bounce, k)
@@ -304,5 +305,6 @@ def render(pack, cam, spp, seed, pixels=None, mode="hybrid", stats=None, trace=N
     if stats is not None:
         stats["nerf_samples"] = int(st["neval"].sum())
         stats["paths"] = len(pix)
+        stats["shadow_rays"] = int(st.get("nshadow", 0))
     assert np.isfinite(out).all() and (out >= 0.0).all()
     return out.reshape(h, w, 3) if pixels is None else out

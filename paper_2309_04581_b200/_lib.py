@@ -77,7 +77,7 @@ class Stats(ctypes.Structure):
                 ("field_ms", ctypes.c_float), ("field_launches", ctypes.c_int32),
                 ("launches", ctypes.c_int64), ("evaluated", ctypes.c_int64),
                 ("rounds", ctypes.c_int64), ("stage_ms", ctypes.c_float * 8),
-                ("batch_rows", ctypes.c_int64)]
+                ("batch_rows", ctypes.c_int64), ("shadow_traced", ctypes.c_int64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}
@@ -119,6 +119,9 @@ SIGNATURES = {
     "hrt_ipc_open": (ctypes.c_int, [vp, ctypes.POINTER(vp)]),
     "hrt_ipc_close": (ctypes.c_int, [vp]),
     "hrt_gather_peak": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
+    "hrt_set_field_transform": (ctypes.c_int, [vp, ctypes.c_int32, vp]),
+    "hrt_l2_peak": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                   ctypes.POINTER(ctypes.c_int64)]),
     "hrt_refit": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "hrt_field_sample": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int32, vp]),
     "hrt_field_encode": (ctypes.c_int, [vp, vp, ctypes.c_int64, vp, vp, vp]),

@@ -190,7 +190,11 @@ struct PathState {
                                               // frame evaluates ~1e11 NeRF samples
 };
 
-enum Stat { S_SAMPLES = 0, S_SHADOW = 1, S_SEGMENTS = 2, S_EVALS = 3, S_ROWS = 4, S_COUNT = 8 };
+// S_SHADOW: shadow rays traced (k_shadow casts one per batch row that needs
+// it, including rows a later early-out / cap discards); S_SHADOW_USED: the
+// ones whose mask was composited (the reference's count, field.py:246-251).
+enum Stat { S_SAMPLES = 0, S_SHADOW = 1, S_SEGMENTS = 2, S_EVALS = 3, S_ROWS = 4, S_SHADOW_USED = 8,
+            S_COUNT = 10 };
 
 HRT_DEV void stat_add(unsigned long long* stats, int which, long long v) {
     atomicAdd(stats + which, (unsigned long long)v);

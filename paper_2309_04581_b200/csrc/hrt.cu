@@ -127,8 +127,11 @@ struct hrt_handle {
     uint32_t* occ_dev = nullptr;
     int64_t occ_words = 0;
     unsigned long long tex = 0;
+    double* rigid_xf = nullptr;     // hrt_refit_rigid: device copy of the per-mesh transforms
+    int32_t rigid_xf_cap = 0;
     double* rigid_base = nullptr;   // hrt_set_rigid_base: object-space corners, global face order
     std::vector<int32_t> mesh_of_host;
+    int32_t n_meshes = 0;           // max(mesh_of) + 1
     int32_t* blk_map = nullptr;     // blocker face -> global face
     int64_t tab_entries = 0;
     int shadow_blocks = 0;
@@ -167,6 +170,7 @@ struct hrt_handle {
         for (cudaEvent_t e : mev) if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : pev) cudaEventDestroy(e);
         if (pinned) cudaFreeHost(pinned);
+        if (rigid_xf) cudaFree(rigid_xf);
         if (io_pix) cudaFree(io_pix);
         if (io_out) cudaFree(io_out);
         if (io_pix_host) cudaFreeHost(io_pix_host);
@@ -766,6 +770,10 @@ int build_occupancy(hrt_handle* h, double thr) {
 
 int ensure_state(hrt_handle* h, int64_t paths) {
     if (paths <= h->cap) return HRT_OK;
+    // the old carve is dead from here on: a failed allocation below must not
+    // leave a capacity that a later smaller render would trust
+    h->cap = 0;
+    h->batch_cap = 0;
     if (h->arena) { cudaFree(h->arena); h->arena = nullptr; }
     const int64_t n = paths;
     const int64_t nb = std::min<int64_t>(n * std::max(kern::kRoundSamples, kern::kRoundSamplesSmall), kBatchCap);
@@ -815,6 +823,7 @@ int ensure_geo(hrt_handle* h, int32_t n_bounces) {
         h->ms.geo.cap = h->cap;
         return HRT_OK;
     }
+    h->geo_n = 0;
     if (h->geo_arena) { cudaFree(h->geo_arena); h->geo_arena = nullptr; }
     const size_t dbl = (size_t)need * 8;
     CK(cudaMalloc(&h->geo_arena, 7 * dbl + (size_t)need * 4));
@@ -833,10 +842,15 @@ int ensure_geo(hrt_handle* h, int32_t n_bounces) {
 // their pinned host staging copies.
 int ensure_io(hrt_handle* h, int64_t npx) {
     if (npx <= h->io_cap) return HRT_OK;
+    h->io_cap = 0;                       // (stale buffers are never trusted after a failed grow)
     if (h->io_pix) cudaFree(h->io_pix);
     if (h->io_out) cudaFree(h->io_out);
     if (h->io_pix_host) cudaFreeHost(h->io_pix_host);
     if (h->io_out_host) cudaFreeHost(h->io_out_host);
+    h->io_pix = nullptr;
+    h->io_out = nullptr;
+    h->io_pix_host = nullptr;
+    h->io_out_host = nullptr;
     const size_t n = (size_t)std::max<int64_t>(npx, 1);
     CK(cudaMalloc(&h->io_pix, n * 4));
     CK(cudaMalloc(&h->io_out, n * 24));
@@ -1153,6 +1167,7 @@ int hrt_create(const hrt_scene_desc* d, hrt_handle** out) {
     if ((rc = upload_bvh(h, h->bvh, sc.bvh, h->rf))) return bail(rc);
     if ((rc = upload_bvh(h, h->blk, sc.blockers, h->rfb))) return bail(rc);
     h->mesh_of_host.assign(d->mesh_of, d->mesh_of + d->n_faces);
+    for (int32_t m : h->mesh_of_host) h->n_meshes = std::max(h->n_meshes, m + 1);
     if ((rc = setup_refit(h, h->bvh, h->rf))) return bail(rc);
     if ((rc = setup_refit(h, h->blk, h->rfb))) return bail(rc);
     double *normal, *emission;
@@ -1308,7 +1323,8 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
     if (stats) {
         stats->paths = total_pix * spp;
         stats->nerf_samples = (int64_t)tot[S_SAMPLES];
-        stats->shadow_rays = (int64_t)tot[S_SHADOW];
+        stats->shadow_rays = (int64_t)tot[S_SHADOW_USED];
+        stats->shadow_traced = (int64_t)tot[S_SHADOW];
         stats->bounce_rays = (int64_t)tot[S_SEGMENTS];
         stats->trace_records = ctr[C_TRACE];
         stats->evaluated = (int64_t)tot[S_EVALS];
@@ -1538,8 +1554,15 @@ int hrt_refit_rigid(hrt_handle* h, const double* xf, int32_t n_meshes) {
     if (!h || !xf) return fail(HRT_EINVAL, "null argument");
     if (!h->rigid_base) return fail(HRT_EINVAL, "hrt_set_rigid_base first");
     if (h->bvh.n_faces == 0) return HRT_OK;
-    double* dxf = nullptr;
-    CK(cudaMalloc(&dxf, (size_t)n_meshes * 12 * 8));
+    if (n_meshes != h->n_meshes) return fail(HRT_EINVAL, "refit_rigid: one 3x4 transform per mesh required");
+    if (n_meshes > h->rigid_xf_cap) {            // persistent transform buffer (grow only)
+        h->rigid_xf_cap = 0;
+        if (h->rigid_xf) cudaFree(h->rigid_xf);
+        h->rigid_xf = nullptr;
+        CK(cudaMalloc(&h->rigid_xf, (size_t)n_meshes * 12 * 8));
+        h->rigid_xf_cap = n_meshes;
+    }
+    double* dxf = h->rigid_xf;
     CK(cudaMemcpy(dxf, xf, (size_t)n_meshes * 12 * 8, cudaMemcpyHostToDevice));
     const int32_t n = h->bvh.n_faces;
     const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
@@ -1554,7 +1577,6 @@ int hrt_refit_rigid(hrt_handle* h, const double* xf, int32_t n_meshes) {
         rc = refit_from_src(h, h->blk, h->rfb, h->sc.blockers);
     }
     CK(cudaDeviceSynchronize());
-    cudaFree(dxf);
     return rc;
 }
 
@@ -1740,6 +1762,61 @@ int hrt_gather_peak(hrt_handle* h, int32_t mode, double* gbs) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaStreamDestroy(s2);
+    cudaFree(sink);
+    return HRT_OK;
+}
+
+int hrt_set_field_transform(hrt_handle* h, int32_t identity, const double* field_from_world) {
+    if (!h || (!identity && !field_from_world)) return fail(HRT_EINVAL, "null argument");
+    if (h->sc.field.kind == HRT_FIELD_NONE) return fail(HRT_EINVAL, "scene has no field");
+    DevField& f = h->sc.field;
+    if (!identity) {
+        if (field_from_world[12] != 0.0 || field_from_world[13] != 0.0 || field_from_world[14] != 0.0 ||
+            field_from_world[15] != 1.0)
+            return fail(HRT_EINVAL, "field_from_world bottom row must be (0,0,0,1)");
+        for (int i = 0; i < 12; ++i) f.inv[i] = field_from_world[i];
+    }
+    f.identity = identity ? 1 : 0;       // (the occupancy grid lives in the field frame: unchanged)
+    return HRT_OK;
+}
+
+int hrt_l2_peak(hrt_handle* h, double* read_gbs, double* sector_gbs, int64_t* bytes) {
+    if (!h || !read_gbs || !sector_gbs) return fail(HRT_EINVAL, "null argument");
+    if (h->sc.field.kind != HRT_FIELD_NEURAL) return fail(HRT_EINVAL, "needs a neural field");
+    const NeuralField& nf = h->sc.field.nf;
+    const int64_t nbytes = (int64_t)h->tab_entries * h->F * 4;
+    const int64_t n16 = nbytes / 16;
+    const uint4* buf = reinterpret_cast<const uint4*>(nf.table);
+    float* sink = nullptr;
+    CK(cudaMalloc(&sink, 4));
+    const int threads = 512, blocks = h->sm_count * 4;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    float ms = 0.f;
+    // coalesced streaming reads of the L2-resident table
+    const int passes = 8;
+    probe::k_l2_read<<<blocks, threads>>>(buf, n16, 1, sink);       // warm: table into L2
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e0, 0));
+    probe::k_l2_read<<<blocks, threads>>>(buf, n16, passes, sink);
+    CK(cudaEventRecord(e1, 0));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    *read_gbs = (double)n16 * 16.0 * passes / (ms * 1e-3) / 1e9;
+    // random 32-B sector gathers over the same table
+    const uint32_t n_sec = (uint32_t)(nbytes / 32);
+    const int iters = 64;
+    probe::k_sector_gather<<<blocks, threads>>>(buf, n_sec, iters, sink);   // warm
+    CK(cudaEventRecord(e0, 0));
+    probe::k_sector_gather<<<blocks, threads>>>(buf, n_sec, iters, sink);
+    CK(cudaEventRecord(e1, 0));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    *sector_gbs = (double)blocks * threads * iters * 8 * 16.0 / (ms * 1e-3) / 1e9;
+    if (bytes) *bytes = nbytes;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
     cudaFree(sink);
     return HRT_OK;
 }

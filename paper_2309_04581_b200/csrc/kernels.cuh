@@ -219,6 +219,7 @@ HRT_DEV void composite(const Args& a, Acc& c, double sigma, const double rgb[3],
     if (needs_shadow(a.sc, al, rgb)) {
         m = path::shadow_mask(a.sc, p, a.seed, pix, smp, a.bounce, k);
         stat_add(a.ps.stats, S_SHADOW, 1);
+        stat_add(a.ps.stats, S_SHADOW_USED, 1);
     }
     const double am = al * m;
     for (int ch = 0; ch < 3; ++ch) c.L[ch] = c.L[ch] + (c.Ts[ch] * am) * rgb[ch];
@@ -586,7 +587,7 @@ constexpr int32_t kCompBatch = HRT_COMP_BATCH;
 
 template <bool kTrace, bool kShadows = true>
 HRT_DEV bool comp_path(const Args& a, const MarchState& m, int32_t p, int32_t j, int32_t nq,
-                       int32_t cnt, double delta, Acc& c, int32_t& done) {
+                       int32_t cnt, double delta, Acc& c, int32_t& done, int32_t& shd) {
     bool stop = false;
     // halted() per sample from a running max(T_spec): every channel is
     // scaled by the same keep >= 0 and rounding is monotonic, so
@@ -615,6 +616,7 @@ HRT_DEV bool comp_path(const Args& a, const MarchState& m, int32_t p, int32_t j,
             const double rgb[3] = {(double)f.y, (double)f.z, (double)f.w};
             const double al = 1.0 - exp(-(double)f.x * delta);
             const double mask = (!kShadows || cb[u] == 0) ? 1.0 : path::mask_of(a.sc, cb[u]);
+            if (kShadows && needs_shadow(a.sc, al, rgb)) ++shd;
             c.neval += 1;
             ++done;
             composite_m(c, al, rgb, mask);
@@ -664,16 +666,17 @@ __global__ void __launch_bounds__(256, HRT_COMP_MINB) k_comp(Args a, MarchState 
     int32_t* next = pick(m.mq, mcur ^ 1);
     int32_t* next_n = &a.ps.counters[C_MQ0 + (mcur ^ 1)];
     const PathState& s = a.ps;
-    int32_t done = 0;
+    int32_t done = 0, shd = 0;
     for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += gridDim.x * blockDim.x) {
         const int32_t p = q[j];
         Acc c;
         load_acc(s, p, c);
-        const bool stop = comp_path<kTrace>(a, m, p, j, nq, m.cnt[p], m.delta[p], c, done);
+        const bool stop = comp_path<kTrace>(a, m, p, j, nq, m.cnt[p], m.delta[p], c, done, shd);
         store_acc(s, p, c);
         if (!stop && !halted(a.sc, c) && m.k[p] < m.n[p]) next[reserve(next_n)] = p;
     }
     if (done) stat_add(a.ps.stats, S_SAMPLES, done);
+    if (shd) stat_add(a.ps.stats, S_SHADOW_USED, shd);
     if (blockIdx.x == 0 && threadIdx.x == 0) stat_add(a.ps.stats, S_EVALS, a.ps.counters[C_NS]);
 }
 
@@ -746,7 +749,7 @@ struct Grp {
 
 template <int G, bool kShadows>
 HRT_DEV bool comp_path_tail(const Args& a, const MarchState& m, int32_t j, int32_t nq, int32_t cnt,
-                            double delta, Acc& c, int32_t& done, const Grp<G>& g) {
+                            double delta, Acc& c, int32_t& done, int32_t& shd, const Grp<G>& g) {
     bool stop = false;
     double tmax = fmax(fmax(c.Ts[0], c.Ts[1]), c.Ts[2]);
     const double early_t = a.sc.early_t;
@@ -770,6 +773,7 @@ HRT_DEV bool comp_path_tail(const Args& a, const MarchState& m, int32_t j, int32
                 } else {
                     c.neval += 1;
                     ++done;
+                    if (kShadows && needs_shadow(a.sc, alu, rgb)) ++shd;
                     composite_m(c, alu, rgb, mu);
                     tmax = tmax * (1.0 - alu);
                 }
@@ -850,7 +854,7 @@ HRT_DEV int32_t gen_path_tail(const Args& a, const MarchState& m, int32_t p, int
 template <int G>
 HRT_DEV void step_tail(const Args& a, const MarchState& m, int32_t first, int32_t S, int32_t prev_nq,
                        int32_t nq, const int32_t* q, int32_t* next, int32_t* next_n, int32_t& done,
-                       int32_t& made, int32_t& held, int32_t& segs) {
+                       int32_t& made, int32_t& held, int32_t& segs, int32_t& shd) {
     const PathState& s = a.ps;
     const Grp<G> g;
     const int32_t groups = (int32_t)(gridDim.x * blockDim.x / G);
@@ -861,8 +865,8 @@ HRT_DEV void step_tail(const Args& a, const MarchState& m, int32_t first, int32_
         int32_t go = 1;
         if (!first) {
             const bool stop = a.sc.em.n > 0
-                                  ? comp_path_tail<G, true>(a, m, m.base[p], prev_nq, m.cnt[p], m.delta[p], c, done, g)
-                                  : comp_path_tail<G, false>(a, m, m.base[p], prev_nq, m.cnt[p], m.delta[p], c, done, g);
+                                  ? comp_path_tail<G, true>(a, m, m.base[p], prev_nq, m.cnt[p], m.delta[p], c, done, shd, g)
+                                  : comp_path_tail<G, false>(a, m, m.base[p], prev_nq, m.cnt[p], m.delta[p], c, done, shd, g);
             if (g.gl == 0) go = !stop && !halted(a.sc, c) && m.k[p] < m.n[p];
         } else if (g.gl == 0) {
             go = m.k[p] < m.n[p];
@@ -910,9 +914,9 @@ __global__ void __launch_bounds__(HRT_STEP_THREADS, HRT_STEP_MINB * 256 / HRT_ST
     int32_t* next = pick(m.mq, mcur ^ 1);
     int32_t* next_n = &a.ps.counters[C_MQ0 + (mcur ^ 1)];
     const PathState& s = a.ps;
-    int32_t done = 0, made = 0, held = 0, segs = 0;
+    int32_t done = 0, made = 0, held = 0, segs = 0, shd = 0;
     if (kMixed && kTailLanes > 1 && ctr[C_TAIL]) {
-        step_tail<kTailLanes>(a, m, first, S, prev_nq, nq, q, next, next_n, done, made, held, segs);
+        step_tail<kTailLanes>(a, m, first, S, prev_nq, nq, q, next, next_n, done, made, held, segs, shd);
     } else
     for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += gridDim.x * blockDim.x) {
         const int32_t p = q[j];
@@ -922,8 +926,8 @@ __global__ void __launch_bounds__(HRT_STEP_THREADS, HRT_STEP_MINB * 256 / HRT_ST
         if (!first) {
             // (no emitters: the shadow codes are all 0, compile the mask out)
             const bool stop = a.sc.em.n > 0
-                                  ? comp_path<false, true>(a, m, p, m.base[p], prev_nq, m.cnt[p], m.delta[p], c, done)
-                                  : comp_path<false, false>(a, m, p, m.base[p], prev_nq, m.cnt[p], m.delta[p], c, done);
+                                  ? comp_path<false, true>(a, m, p, m.base[p], prev_nq, m.cnt[p], m.delta[p], c, done, shd)
+                                  : comp_path<false, false>(a, m, p, m.base[p], prev_nq, m.cnt[p], m.delta[p], c, done, shd);
             go = !stop && !halted(a.sc, c) && m.k[p] < m.n[p];
         } else if (kMixed) {
             go = m.k[p] < m.n[p];
@@ -941,6 +945,7 @@ __global__ void __launch_bounds__(HRT_STEP_THREADS, HRT_STEP_MINB * 256 / HRT_ST
         }
     }
     warp_stat_add(a.ps.stats, S_SAMPLES, done);
+    if (a.sc.em.n > 0) warp_stat_add(a.ps.stats, S_SHADOW_USED, shd);
     warp_stat_add(a.ps.stats, S_EVALS, made);
     if (kMixed) warp_stat_add(a.ps.stats, S_SEGMENTS, segs);
     // the host stops the rounds when a round's C_NS is 0: samples made, or

@@ -32,3 +32,46 @@ __global__ void __launch_bounds__(512) k_gather(const float2* __restrict__ table
 }
 
 }  // namespace probe
+
+namespace probe {
+
+// L2 read roofline (hrt_l2_peak): every SM streams an L2-resident buffer
+// (the hash table itself, after a warm pass) with coalesced 16-B loads.
+__global__ void __launch_bounds__(512) k_l2_read(const uint4* __restrict__ buf, int64_t n16,
+                                                  int32_t passes, float* sink) {
+    uint32_t acc = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int32_t p = 0; p < passes; ++p) {
+        int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        for (; i + 3 * stride < n16; i += 4 * stride) {
+            const uint4 a = __ldcg(buf + i), b = __ldcg(buf + i + stride);
+            const uint4 c = __ldcg(buf + i + 2 * stride), d = __ldcg(buf + i + 3 * stride);
+            acc ^= a.x ^ b.y ^ c.z ^ d.w;
+        }
+        for (; i < n16; i += stride) acc ^= __ldcg(buf + i).x;
+    }
+    if (acc == 0x12345678u) sink[0] = (float)acc;
+}
+
+// Random whole-sector gathers: lane pairs read the two 16-B halves of one
+// random 32-B sector of the buffer (16 sectors per warp instruction, L1
+// bypassed), 8 instructions in flight per thread.
+__global__ void __launch_bounds__(512) k_sector_gather(const uint4* __restrict__ buf, uint32_t n_sectors,
+                                                        int32_t iters, float* sink) {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t half = tid & 1u;
+    uint32_t acc = 0;
+    for (int32_t it = 0; it < iters; ++it) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t s = mix32((tid >> 1) * 0x9E3779B9U + (uint32_t)(it * 8 + u)) % n_sectors;
+            v[u] = __ldcg(buf + 2ull * s + half);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc ^= v[u].x ^ v[u].w;
+    }
+    if (acc == 0x12345678u) sink[0] = (float)acc;
+}
+
+}  // namespace probe

@@ -136,6 +136,16 @@ class Renderer:
         _lib.check(self.lib.hrt_refit(self.handle, *ptrs), "hrt_refit")
         self.pack = pk
 
+    def set_field_transform(self, field):
+        """Upload a moved field's placement (hrt_set_field_transform)."""
+        from .pack import _transform_arrays
+        ident, inv = _transform_arrays(field.world_from_field)
+        inv = np.ascontiguousarray(inv, np.float64).reshape(16)
+        _lib.check(self.lib.hrt_set_field_transform(self.handle, int(ident), inv.ctypes.data_as(ctypes.c_void_p)),
+                   "hrt_set_field_transform")
+        self.pack["field"]["identity"] = ident
+        self.pack["field"]["field_from_world"] = inv.reshape(4, 4)
+
     def set_rigid_base(self, object_vertices, indices, emissive=None):
         """Object-space geometry for refit_rigid: per mesh (in scene order) its
         object vertices and faces; `emissive` flags exclude meshes from the
@@ -224,6 +234,14 @@ class Renderer:
         _lib.check(self.lib.hrt_gather_peak(self.handle, int(mode), ctypes.byref(v)), "hrt_gather_peak")
         return v.value
 
+    def l2_peak(self):
+        """Measured L2 roofline over this scene's hash table (hrt_l2_peak):
+        coalesced read GB/s and random 32-B sector-gather GB/s."""
+        rd, sec, nb = ctypes.c_double(0.0), ctypes.c_double(0.0), ctypes.c_int64(0)
+        _lib.check(self.lib.hrt_l2_peak(self.handle, ctypes.byref(rd), ctypes.byref(sec), ctypes.byref(nb)),
+                   "hrt_l2_peak")
+        return {"read_gbs": rd.value, "gather_sector_gbs": sec.value, "bytes": nb.value}
+
     def set_trace(self, records, cap):
         _lib.check(self.lib.hrt_set_trace(self.handle, _dptr(records), int(cap)), "hrt_set_trace")
 
@@ -250,9 +268,14 @@ def primary_rays(camera, pixel, sample, seed, spp):
 
 # ------------------------------------------------------------------ cache
 
-def _geometry_key(scene):
-    # own Scene: explicit version; reference Scene: rebuild_bvh swaps the Bvh
-    return getattr(scene, "version", None), id(getattr(scene, "bvh", None))
+def _field_key(scene):
+    """The field placement the handle must use (reference dynamic fields move
+    by reassigning world_from_field between frames, sim.py:673-698, with no
+    BVH rebuild)."""
+    f = getattr(scene, "field", None)
+    if f is None:
+        return None
+    return np.asarray(f.world_from_field.m, np.float64).tobytes()
 
 
 def _config_of(pack):
@@ -266,23 +289,56 @@ def _scene_config(scene, spawn_eps):
             int(getattr(rc, "sample_cap", 0) or 0), float(getattr(rc, "early_t", 0.0) or 0.0))
 
 
+class _Cached:
+    """A scene's renderer plus what it was uploaded from: this package's
+    `Scene.version`, the reference Scene's Bvh OBJECT (held, compared with
+    `is`: `rebuild_bvh` swaps it, and an id() could be reused once the old
+    one is freed) and the field placement bytes."""
+
+    def __init__(self, scene, r, dev):
+        self.r, self.dev = r, dev
+        self.stamp(scene)
+
+    def stamp(self, scene):
+        self.version = getattr(scene, "version", None)
+        self.bvh = getattr(scene, "bvh", None)
+        self.field = _field_key(scene)
+
+    def geometry_changed(self, scene):
+        return getattr(scene, "version", None) != self.version or getattr(scene, "bvh", None) is not self.bvh
+
+
 def renderer_for(scene) -> Renderer:
-    """The scene's cached renderer: geometry changes refit, RenderConfig
-    changes (read at every call, as the reference does) are pushed with
+    """The scene's cached renderer: geometry changes refit, a moved field
+    re-uploads its placement (hrt_set_field_transform), RenderConfig changes
+    (read at every call, as the reference does) are pushed with
     hrt_set_config."""
     cached = getattr(scene, "_hrt_renderer", None)
-    key = _geometry_key(scene)
     dev = torch.cuda.current_device()
-    if cached is not None and cached[2] == dev:
-        r = cached[1]
-        if cached[0] != key:
+    if cached is not None and cached.dev == dev:
+        r = cached.r
+        if cached.geometry_changed(scene):
             r.refit(scene)
-            scene._hrt_renderer = (key, r, dev)
+        fk = _field_key(scene)
+        if fk != cached.field:
+            r.set_field_transform(scene.field)
+        cached.stamp(scene)
     else:
         r = Renderer(scene)
-        scene._hrt_renderer = (key, r, dev)
+        scene._hrt_renderer = _Cached(scene, r, dev)
     r.set_config(_scene_config(scene, r.pack["spawn_eps"]))
     return r
+
+
+def _image(scene, pixels):
+    """`hybridrt.images.HdrImage` for a reference Scene (so the reference's
+    render and this one return the same type), else this package's."""
+    if type(scene).__module__.startswith("hybridrt"):
+        import sys
+        mod = sys.modules.get("hybridrt.images")
+        if mod is not None:
+            return mod.HdrImage(pixels)
+    return HdrImage(pixels)
 
 
 def _resolve(scene, camera, spp, seed):
@@ -299,7 +355,7 @@ def _frame(scene, camera, spp, seed, mode):
     r = renderer_for(scene)
     out = r.render_pixels(camera, spp, seed, mode)
     w, h = camera.resolution
-    return HdrImage(out.cpu().numpy().reshape(h, w, 3))
+    return _image(scene, out.cpu().numpy().reshape(h, w, 3))
 
 
 def render(scene, camera=None, spp=None, seed=None, threads=1) -> HdrImage:

@@ -236,3 +236,33 @@ def test_gpu_continuous_march_edge_configs(cuda, n_bounces, threshold, sample_ca
     if sample_cap == 1:
         assert sa["nerf_samples"] <= 2 * pix.numel()
     r.close()
+
+
+@pytest.mark.parametrize("sample_cap,early_t,threshold", [
+    (1, 1e-4, 1e-4),             # cap reached on the first sample of the path
+    (37, 1e-4, 1e-4),            # cap inside a round and inside a bounce
+    (0, 0.6, 1e-4),              # in-march early-out after a few samples, shading continues
+    (1024, 1e-4, 0.5),           # post-bounce throughput threshold kills paths at the first hit
+])
+def test_gpu_march_limits_vs_oracle(cuda, sample_cap, early_t, threshold):
+    """SURVEY P5 limits (1024-sample cap, in-march early-out) against the
+    ORACLE's own implementation of them (oracle/tracer.py march), not only
+    against the GPU's bounce loop: images within 1e-3, NeRF sample counts
+    equal."""
+    scene = moving_scene(5)
+    scene.render.sample_cap, scene.render.early_t, scene.render.threshold = sample_cap, early_t, threshold
+    r = Renderer(scene)
+    assert (r.pack["sample_cap"], r.pack["early_t"], r.pack["threshold"]) == (sample_cap, early_t, threshold)
+    w, h = scene.camera.resolution
+    pix = crop(w, h, 16, cx=48, cy=32)
+    got = r.render_pixels(scene.camera, 2, 9,
+                          pixels=torch.as_tensor(pix.astype(np.int32), device=cuda)).cpu().numpy()
+    stats = dict(r.last_stats)
+    st = {}
+    want = tracer.render(r.pack, pack_camera(scene.camera), 2, 9, pixels=pix, stats=st)
+    assert stats["nerf_samples"] == st["nerf_samples"]
+    assert np.abs(got - want).max() < 1e-3
+    if sample_cap == 1:
+        assert st["nerf_samples"] <= 2 * len(pix)
+    assert want.max() > 0.01
+    r.close()
