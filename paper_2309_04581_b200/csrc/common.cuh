@@ -12,6 +12,28 @@
 
 #define HRT_DEV __device__ __forceinline__
 
+// Checked builds (-DHRT_CHECKS=1, tools/build_checked.sh): device-side bounds
+// checks on every queue reservation, batch row, shadow-queue slot and output
+// pixel; a violation prints its site and traps (the launch fails with an
+// error instead of corrupting memory). compute-sanitizer is not available on
+// the GPU pool, so this build is the race / bounds evidence.
+#ifndef HRT_CHECKS
+#define HRT_CHECKS 0
+#endif
+#if HRT_CHECKS
+#include <cstdio>
+#define HRT_ASSERT(cond, what, v, cap)                                                            \
+    do {                                                                                          \
+        if (!(cond)) {                                                                            \
+            printf("HRT_CHECKS %s:%d %s: %lld outside [0, %lld)\n", __FILE__, __LINE__, what,     \
+                   (long long)(v), (long long)(cap));                                             \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define HRT_ASSERT(cond, what, v, cap) do { } while (0)
+#endif
+
 // ----------------------------------------------------------------- vectors
 struct d3 { double x, y, z; };
 HRT_DEV d3 mk(double x, double y, double z) { return {x, y, z}; }

@@ -17,6 +17,7 @@
 #include "bvh_build.h"
 #include "kernels.cuh"
 #include "probe.cuh"
+#include <nvtx3/nvToolsExt.h>
 #include "finalize.cuh"
 
 namespace {
@@ -812,6 +813,8 @@ int ensure_state(hrt_handle* h, int64_t paths) {
     }
     h->cap = n;
     h->batch_cap = nb;
+    h->ms.rows_cap = nb;
+    h->ms.paths_cap = n;
     return HRT_OK;
 }
 
@@ -933,10 +936,17 @@ void prof_fold(hrt_handle* h, cudaStream_t st) {
     }
     h->pn = 0;
 }
-inline void pbeg(hrt_handle* h, cudaStream_t st) {
+// NVTX ranges around every stage's enqueue (named as hrt.h HRT_STAGE_*), so
+// an nsys / ncu --nvtx timeline groups the wavefront's launches by stage;
+// without an attached tool nvtx3 calls are a null-pointer check.
+const char* const kStageName[8] = {"hrt:raygen", "hrt:intersect", "hrt:march_gen", "hrt:field",
+                                   "hrt:shadow", "hrt:composite", "hrt:shade", "hrt:accumulate"};
+inline void pbeg(hrt_handle* h, cudaStream_t st, int stage) {
+    nvtxRangePushA(kStageName[stage]);
     if (h->prof) cudaEventRecord(h->pev[2 * h->pn], st);
 }
 inline void pend(hrt_handle* h, int stage, cudaStream_t st) {
+    nvtxRangePop();
     if (!h->prof) return;
     cudaEventRecord(h->pev[2 * h->pn + 1], st);
     h->pstage[h->pn++] = stage;
@@ -972,7 +982,7 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
         // Rounds are enqueued kRoundsPerCheck at a time; the host then checks
         // whether the last round generated any sample (rounds after the end
         // are empty launches).
-        pbeg(h, st);
+        pbeg(h, st, HRT_STAGE_MARCH_GEN);
         kern::k_march_begin<<<1, 1, 0, st>>>(h->ps.counters);
         kern::k_seg<<<g, kThreads, 0, st>>>(a, h->ms);
         CK(cudaGetLastError());
@@ -983,19 +993,19 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
         const unsigned gsh = (unsigned)(h->sm_count * 16);
         while (true) {
             for (int k = 0; k < kRoundsPerCheck; ++k) {
-                pbeg(h, st);
+                pbeg(h, st, HRT_STAGE_COMPOSITE);
                 kern::k_round_begin<<<1, 1, 0, st>>>(h->ps.counters, h->ps.stats, target, cap);
                 if (a.mixed) kern::k_step<true><<<gs, kStepThreads, 0, st>>>(a, h->ms);
                 else kern::k_step<false><<<gs, kStepThreads, 0, st>>>(a, h->ms);
                 CK(cudaGetLastError());
                 pend(h, HRT_STAGE_COMPOSITE, st);
-                pbeg(h, st);
+                pbeg(h, st, HRT_STAGE_FIELD);
                 if ((rc = field_ws(h, h->ms.in, fws::RowMap{}, 0, h->ms.dir32, h->ms.out, 0, st,
                                    h->ps.counters)))
                     return rc;
                 pend(h, HRT_STAGE_FIELD, st);
                 if (h->sc.em.n > 0) {
-                    pbeg(h, st);
+                    pbeg(h, st, HRT_STAGE_SHADOW);
                     kern::k_shadow<<<gsh, kThreads, 0, st>>>(a, h->ms, fws::RowMap{}, 0, 1);
                     CK(cudaGetLastError());
                     if ((rc = shadow_trace(h, a, st))) return rc;
@@ -1011,7 +1021,7 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
         }
         return HRT_OK;
     }
-    pbeg(h, st);
+    pbeg(h, st, HRT_STAGE_MARCH_GEN);
     kern::k_round_reset<<<1, 1, 0, st>>>(h->ps.counters, 0);
     kern::k_seg<<<g, kThreads, 0, st>>>(a, h->ms);
     CK(cudaGetLastError());
@@ -1023,26 +1033,26 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
     while (live > 0) {
         const int32_t S = round_samples(h, live);
         const unsigned gl = grid_for(h, live);
-        pbeg(h, st);
+        pbeg(h, st, HRT_STAGE_MARCH_GEN);
         kern::k_round_reset<<<1, 1, 0, st>>>(h->ps.counters, mc ^ 1);
         kern::k_gen<<<gl, kThreads, 0, st>>>(a, h->ms, mc, S);
         CK(cudaGetLastError());
         pend(h, HRT_STAGE_MARCH_GEN, st);
-        pbeg(h, st);
+        pbeg(h, st, HRT_STAGE_FIELD);
         if ((rc = field_ws(h, h->ms.in, fws::RowMap{}, (int64_t)live * S, h->ms.dir32, h->ms.out, 0,
                            st)))
             return rc;
         pend(h, HRT_STAGE_FIELD, st);
         if (h->sc.em.n > 0) {
             const int64_t rows = (int64_t)live * S;
-            pbeg(h, st);
+            pbeg(h, st, HRT_STAGE_SHADOW);
             kern::k_shadow<<<grid_for(h, rows), kThreads, 0, st>>>(a, h->ms, fws::RowMap{}, rows, 0);
             CK(cudaGetLastError());
             if ((rc = shadow_trace(h, a, st))) return rc;
             pend(h, HRT_STAGE_SHADOW, st);
             ++h->launches;
         }
-        pbeg(h, st);
+        pbeg(h, st, HRT_STAGE_COMPOSITE);
         if (a.trace) kern::k_comp<true><<<gl, kThreads, 0, st>>>(a, h->ms, mc);
         else kern::k_comp<false><<<gl, kThreads, 0, st>>>(a, h->ms, mc);
         CK(cudaGetLastError());
@@ -1057,7 +1067,7 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
 
 int march(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream_t st) {
     if (h->sc.field.kind == HRT_FIELD_DENSE) {
-        pbeg(h, st);
+        pbeg(h, st, HRT_STAGE_COMPOSITE);
         kern::k_march_dense<<<grid_for(h, n_paths), kThreads, 0, st>>>(a);
         CK(cudaGetLastError());
         pend(h, HRT_STAGE_COMPOSITE, st);
@@ -1090,7 +1100,7 @@ int run_bounces(hrt_handle* h, kern::Args& a, int64_t paths, int mode, cudaStrea
         a.cur = 0;
         a.mixed = 1;
         if ((rc = ensure_geo(h, h->sc.n_bounces))) return rc;
-        pbeg(h, st);
+        pbeg(h, st, HRT_STAGE_INTERSECT);
         kern::k_reset_queue<<<1, 1, 0, st>>>(h->ps.counters, 1);
         if (paths < kCoopPaths) kern::k_paths_coop<<<grid_for(h, paths * 4), kThreads, 0, st>>>(a, h->ms.geo);
         else kern::k_paths<<<(unsigned)std::min<int64_t>((paths + HRT_PATHS_THREADS - 1) / HRT_PATHS_THREADS,
@@ -1104,13 +1114,13 @@ int run_bounces(hrt_handle* h, kern::Args& a, int64_t paths, int mode, cudaStrea
     for (int b = 1; b <= h->sc.n_bounces; ++b) {
         a.bounce = b;
         a.cur = (b - 1) & 1;
-        pbeg(h, st);
+        pbeg(h, st, HRT_STAGE_INTERSECT);
         kern::k_reset_queue<<<1, 1, 0, st>>>(h->ps.counters, a.cur ^ 1);
         kern::k_intersect<<<g, kThreads, 0, st>>>(a);
         CK(cudaGetLastError());
         pend(h, HRT_STAGE_INTERSECT, st);
         if (field && mode == HRT_MODE_HYBRID && (rc = march(h, a, paths, st))) return rc;
-        pbeg(h, st);
+        pbeg(h, st, HRT_STAGE_SHADE);
         kern::k_shade<<<g, kThreads, 0, st>>>(a);
         CK(cudaGetLastError());
         pend(h, HRT_STAGE_SHADE, st);
@@ -1301,13 +1311,13 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
         a.out_by_pixel = by_pixel;
         a.trace = h->trace;
         a.trace_cap = h->trace_cap;
-        pbeg(h, st);
+        pbeg(h, st, HRT_STAGE_RAYGEN);
         kern::k_raygen<<<grid_for(h, paths), kThreads, 0, st>>>(a);
         CK(cudaGetLastError());
         pend(h, HRT_STAGE_RAYGEN, st);
         h->launches += 2;   // raygen + accumulate
         if ((rc = run_bounces(h, a, paths, mode, st))) return rc;
-        pbeg(h, st);
+        pbeg(h, st, HRT_STAGE_ACCUMULATE);
         kern::k_accumulate<<<grid_for(h, np), kThreads, 0, st>>>(a);
         CK(cudaGetLastError());
         pend(h, HRT_STAGE_ACCUMULATE, st);

@@ -335,7 +335,12 @@ struct MarchState {         // per path, valid while the path is marching
     uint64_t* h4;           // per path: rng::prefix(seed, pix, smp, bounce) of this bounce
     int32_t* bounce;        // per path: its current bounce (continuous wavefront march)
     PathGeo geo;            // per path and bounce: ray + nearest hit (k_paths)
+    int64_t rows_cap;       // batch rows allocated (HRT_CHECKS)
+    int64_t paths_cap;      // path slots allocated (HRT_CHECKS)
 };
+
+#define HRT_CHECK_ROW(m, row) HRT_ASSERT((row) >= 0 && (row) < (m).rows_cap, "batch row", row, (m).rows_cap)
+#define HRT_CHECK_SLOT(m, r) HRT_ASSERT((r) >= 0 && (r) < (m).paths_cap, "queue slot", r, (m).paths_cap)
 
 // A queued shadow ray (64 B): origin = the NeRF sample point, float64 as the
 // reference; row of the batch sample it decides.
@@ -557,6 +562,7 @@ HRT_DEV int32_t gen_path(const Args& a, const MarchState& m, int32_t p, int32_t 
                 const float3 p32 = nerf::to_f32(xf);
                 fws::SampleIn r;
                 r.x = p32.x; r.y = p32.y; r.z = p32.z; r.path = p;
+                HRT_CHECK_ROW(m, (int64_t)cnt * nq + j);
                 st_row(&m.in[(int64_t)cnt * nq + j], r);
                 if (a.sc.em.n > 0 || a.trace) m.sk[(int64_t)cnt * nq + j] = k;   // read by shadows / trace only
                 ++cnt;
@@ -570,6 +576,7 @@ HRT_DEV int32_t gen_path(const Args& a, const MarchState& m, int32_t p, int32_t 
         fws::SampleIn r;
         r.x = r.y = r.z = 0.f;
         r.path = -1;
+        HRT_CHECK_ROW(m, (int64_t)i * nq + j);
         st_row(&m.in[(int64_t)i * nq + j], r);
     }
     m.cnt[p] = cnt;
@@ -812,6 +819,7 @@ HRT_DEV int32_t gen_path_tail(const Args& a, const MarchState& m, int32_t p, int
                 fws::SampleIn r;
                 r.x = p32.x; r.y = p32.y; r.z = p32.z; r.path = p;
                 const int64_t row = (int64_t)(cnt + rank) * nq + j;
+                HRT_CHECK_ROW(m, row);
                 st_row(&m.in[row], r);
                 if (write_k) m.sk[row] = kk;
             }
@@ -841,6 +849,7 @@ HRT_DEV int32_t gen_path_tail(const Args& a, const MarchState& m, int32_t p, int
         fws::SampleIn r;
         r.x = r.y = r.z = 0.f;
         r.path = -1;
+        HRT_CHECK_ROW(m, (int64_t)i * nq + j);
         st_row(&m.in[(int64_t)i * nq + j], r);
     }
     if (g.gl == 0) {
@@ -886,6 +895,7 @@ HRT_DEV void step_tail(const Args& a, const MarchState& m, int32_t first, int32_
             int32_t r = 0;
             if (g.gl == 0) {
                 r = reserve(next_n);
+                HRT_CHECK_SLOT(m, r);
                 next[r] = p;
                 m.base[p] = r;
             }
@@ -938,6 +948,7 @@ __global__ void __launch_bounds__(HRT_STEP_THREADS, HRT_STEP_MINB * 256 / HRT_ST
             // dense next batch: rank r among the paths that go on; rows
             // i * nq + r (the field engine reads them through a RowMap)
             const int32_t r = reserve(next_n);
+            HRT_CHECK_SLOT(m, r);
             next[r] = p;
             m.base[p] = r;
             made += gen_path(a, m, p, r, nq, S, c);
@@ -995,7 +1006,9 @@ __global__ void __launch_bounds__(256, HRT_SHADOW_MINB) k_shadow(Args a, MarchSt
                     q.tmax = r.tmax;
                     q.row = (int32_t)row;
                     q.idx = r.idx;
-                    m.shq[reserve(&a.ps.counters[C_SHQ])] = q;
+                    const int32_t qs = reserve(&a.ps.counters[C_SHQ]);
+                    HRT_CHECK_ROW(m, qs);
+                    m.shq[qs] = q;
                     code = -1;                         // decided by k_shadow_trace
                 }
             } else {
@@ -1321,7 +1334,10 @@ __global__ void k_accumulate(Args a) {
         }
         // (out_by_pixel: a raster frame, possibly rank 0's mapped over NVLink - the
         // frame "gather" is these stores, issued as each chunk's pixels finish)
-        double* o = a.out + 3 * ((a.tiled || a.out_by_pixel) ? slot_pixel(a, slot) : a.out_offset + slot);
+        const int64_t oi = (a.tiled || a.out_by_pixel) ? slot_pixel(a, slot) : a.out_offset + slot;
+        HRT_ASSERT(oi >= 0 && (!(a.tiled || a.out_by_pixel) || oi < (int64_t)a.cam.width * a.cam.height),
+                   "output pixel", oi, (int64_t)a.cam.width * a.cam.height);
+        double* o = a.out + 3 * oi;
         bool bad = false;
         for (int ch = 0; ch < 3; ++ch) {
             const double v = acc[ch] / (double)a.spp;
