@@ -1366,7 +1366,8 @@ __global__ void k_field_prep(DevField fld, const double* __restrict__ pts,
         }
         fws::SampleIn r;
         const float3 p32 = nerf::to_f32(pf);
-        r.x = p32.x; r.y = p32.y; r.z = p32.z; r.path = (int32_t)i;
+        r.x = p32.x; r.y = p32.y; r.z = p32.z;
+        r.path = e ? (int32_t)i : -1;      // the engine evaluates inside (occupied) points only
         in[i] = r;
         if (dirs) {
             const d3 df = field_dir(fld, mk(dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]));
