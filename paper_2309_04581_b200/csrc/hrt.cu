@@ -130,6 +130,7 @@ struct hrt_handle {
     unsigned long long tex = 0;
     double* rigid_xf = nullptr;     // hrt_refit_rigid: device copy of the per-mesh transforms
     int32_t rigid_xf_cap = 0;
+    bool blk_stale = false;         // blocker forest behind the last hrt_refit_rigid (no emitters)
     double* rigid_base = nullptr;   // hrt_set_rigid_base: object-space corners, global face order
     std::vector<int32_t> mesh_of_host;
     int32_t n_meshes = 0;           // max(mesh_of) + 1
@@ -1509,6 +1510,7 @@ int hrt_refit(hrt_handle* h, const double* v0, const double* e1, const double* e
     }
     if (h->blk.n_faces && bv0 && be1 && be2) {
         if ((rc = refit_gpu(h, h->blk, h->rfb, h->sc.blockers, bv0, be1, be2))) return rc;
+        h->blk_stale = false;
     }
     CK(cudaDeviceSynchronize());
     return HRT_OK;
@@ -1560,6 +1562,18 @@ int hrt_set_rigid_base(hrt_handle* h, const double* corners, const int32_t* bloc
     return HRT_OK;
 }
 
+// Blocker forest refit from the current rigid-moved faces (hrt_refit_rigid).
+static int ensure_blockers(hrt_handle* h) {
+    if (!h->blk_stale) return HRT_OK;
+    const int32_t n = h->bvh.n_faces, nb = h->blk.n_faces;
+    const unsigned gb = (unsigned)std::min<int64_t>((nb + 255) / 256, 148 * 16);
+    bvh::k_gather_faces<<<gb, 256>>>(h->rf.src, n, h->blk_map, nb, h->rfb.src);
+    CK(cudaGetLastError());
+    const int rc = refit_from_src(h, h->blk, h->rfb, h->sc.blockers);
+    if (rc == HRT_OK) h->blk_stale = false;
+    return rc;
+}
+
 int hrt_refit_rigid(hrt_handle* h, const double* xf, int32_t n_meshes) {
     if (!h || !xf) return fail(HRT_EINVAL, "null argument");
     if (!h->rigid_base) return fail(HRT_EINVAL, "hrt_set_rigid_base first");
@@ -1579,12 +1593,11 @@ int hrt_refit_rigid(hrt_handle* h, const double* xf, int32_t n_meshes) {
     bvh::k_rigid_faces<<<g, 256>>>(h->rigid_base, h->sc.mesh_of, dxf, n_meshes, n, h->rf.src, h->d_normal);
     CK(cudaGetLastError());
     int rc = refit_from_src(h, h->bvh, h->rf, h->sc.bvh);
+    // the shadow-blocker forest is only traversed by shadow rays: without
+    // emitters its refit waits until something queries it (hrt_intersect)
     if (rc == HRT_OK && h->blk.n_faces) {
-        const int32_t nb = h->blk.n_faces;
-        const unsigned gb = (unsigned)std::min<int64_t>((nb + 255) / 256, 148 * 16);
-        bvh::k_gather_faces<<<gb, 256>>>(h->rf.src, n, h->blk_map, nb, h->rfb.src);
-        CK(cudaGetLastError());
-        rc = refit_from_src(h, h->blk, h->rfb, h->sc.blockers);
+        h->blk_stale = true;
+        if (h->sc.em.n > 0) rc = ensure_blockers(h);
     }
     CK(cudaDeviceSynchronize());
     return rc;
@@ -1634,6 +1647,10 @@ int hrt_intersect(hrt_handle* h, int32_t blocker, int32_t any, const double* o, 
     if (!h || (n > 0 && (!o || !d))) return fail(HRT_EINVAL, "null argument");
     if (any ? !hit : (!t || !face)) return fail(HRT_EINVAL, "missing output");
     if (n == 0) return HRT_OK;
+    if (blocker) {
+        int rc;
+        if ((rc = ensure_blockers(h))) return rc;
+    }
     const DevBvh& b = blocker ? h->sc.blockers : h->sc.bvh;
     kern::k_rays<<<grid_for(h, n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         b, o, d, t_min, t_max, n, any, t, face, hit);
