@@ -143,3 +143,32 @@ def test_render_rejects_bad_spp_before_touching_the_gpu():
     from paper_2309_04581_b200 import render
     with pytest.raises(ValueError):
         render(configs.cfg0(), spp=0)
+
+
+def test_renderer_cache_tracks_bvh_object_and_field_placement(hybridrt):
+    """renderer_for's cache key: a reference Scene's Bvh OBJECT
+    (held and compared with `is`, so a freed-and-reused id() cannot hide a
+    rebuild) and the field placement bytes (a dynamic field moves without a
+    BVH rebuild, sim.py:673-698)."""
+    import importlib
+    from paper_2309_04581_b200.renderer import _Cached, _field_key
+    rs = importlib.import_module("hybridrt.scene")
+    rf = importlib.import_module("hybridrt.field")
+    sf = importlib.import_module("hybridrt.surface")
+    rr = importlib.import_module("hybridrt.render")
+    core = importlib.import_module("hybridrt.core")
+    v = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], float)
+    mesh = sf.TriangleMesh(v, [[0, 1, 2]], sf.Lambertian((0.5, 0.5, 0.5)))
+    field = rf.RadianceGrid.constant((0, 0, 0), (1, 1, 1), 1.0, (1, 1, 1))
+    bvh = sf.Bvh([mesh])
+    cam = rr.Camera(core.Transform.look_at((0, 0, 3), (0, 0, 0)), 0.5, (4, 4))
+    scene = rs.Scene(config=None, camera=cam, render=rs.RenderConfig(), field=field, meshes=[mesh],
+                     bvh=bvh, blocker_bvh=bvh, emitters=None, collider_sdfs=[], spawn_eps=1e-4)
+    c = _Cached(scene, None, 0)
+    assert not c.geometry_changed(scene) and _field_key(scene) == c.field
+    scene.rebuild_bvh()
+    assert c.geometry_changed(scene)
+    c.stamp(scene)
+    assert not c.geometry_changed(scene)
+    scene.field.world_from_field = core.Transform.translate((0.1, 0.0, 0.0))
+    assert _field_key(scene) != c.field and not c.geometry_changed(scene)
