@@ -32,19 +32,23 @@ def ref():
 
 def test_field_hit_simulation_frames(ref, tmp_path, cuda):
     """The reference's field-hit preset (a ball flying into a rigid radiance
-    blob) through 4 simulated frames: every frame the GPU image equals the
+    blob, the cli.py:132-171 frame loop) through 40 simulated frames,
+    rendered every 8th: each rendered frame the GPU image equals the
     reference's render of the same Scene (dense grid: float64 end to end),
-    the result is the reference's HdrImage type, one uploaded renderer is
-    refit (Bvh swapped by rebuild_bvh) and re-placed (the field moves)."""
+    the result is the reference's HdrImage type, and one uploaded renderer
+    is refit (Bvh swapped by rebuild_bvh) and re-placed (the blob is hit
+    and moves from frame ~20 on)."""
     path = ref["assets"].generate("field-hit", str(tmp_path))[0]
     scene = ref["scene"].load_scene(path)
     world, binding = ref["sim"].build_world(scene)
     cfg = scene.config.sim
     renderer, field0 = None, scene.field.world_from_field.m.copy()
-    for k in range(4):
+    for k in range(41):
         if k:
             ref["sim"].step(world, cfg.dt, cfg.substeps, cfg.iterations)
             ref["sim"].sync_to_renderer(world, scene, binding)
+        if k % 8:
+            continue
         got = hrt.render(scene, spp=2, seed=6)
         want = ref["render"].render(scene, spp=2, seed=6)
         assert type(got) is ref["images"].HdrImage
