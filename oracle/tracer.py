@@ -297,10 +297,21 @@ def render(pack, cam, spp, seed, pixels=None, mode="hybrid", stats=None, trace=N
     o, d = primary_rays(cam, pix, jx, jy)
     st = new_state(len(pix))
     L = trace_paths(sc, o, d, pix, smp, seed, mode=mode, st=st, trace=trace)
+    # per-pixel sums grouped as the reference's batches (render.py:333-350):
+    # a 16-row band of npix = rows * w pixels takes max(1, 65536 // npix)
+    # samples per batch, each batch summed with .sum(axis=1), then added
     acc = np.zeros((len(pix_list), 3))
     Lr = L.reshape(len(pix_list), spp, 3)
-    for s in range(spp):
-        acc += Lr[:, s]
+    row = pix_list // w
+    band = row - row % 16
+    per_batch = np.maximum(1, 65536 // (np.minimum(16, h - band) * w))
+    for pb in np.unique(per_batch):
+        sel = per_batch == pb
+        s = 0
+        while s < spp:
+            sb = min(int(pb), spp - s)
+            acc[sel] += Lr[sel, s:s + sb].sum(axis=1)
+            s += sb
     out = acc / spp
     if stats is not None:
         stats["nerf_samples"] = int(st["neval"].sum())

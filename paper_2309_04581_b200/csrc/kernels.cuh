@@ -1321,20 +1321,39 @@ __global__ void k_reset_queue(int32_t* counters, int32_t which) {
 }
 
 // Per-pixel sum over its spp paths in sample order, then / spp (render.py:348-350).
+// Per-pixel sum in the reference's grouping (render.py:333-350): a 16-row
+// band of npix = rows * w pixels is traced in batches of
+// max(1, 65536 // npix) samples per pixel, each batch summed over its
+// samples left to right (`L.reshape(npix, sb, 3).sum(axis=1)`, a sequential
+// reduce in numpy), then added to the band's accumulator - so for frames
+// wider than 4096 / spp the sums group exactly as the reference's do.
 __global__ void k_accumulate(Args a) {
     const PathState& s = a.ps;
+    const int64_t W = a.cam.width, H = a.cam.height;
     for (int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; slot < a.n_slots;
          slot += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t pix = slot_pixel(a, slot);
+        const int64_t row = pix / W, band = row - row % 16;
+        const int64_t npix = min((int64_t)16, H - band) * W;
+        const int32_t per_batch = (int32_t)max((int64_t)1, (int64_t)65536 / npix);
         double acc[3] = {0.0, 0.0, 0.0};
-        for (int32_t k = 0; k < a.spp; ++k) {
-            const int64_t p = slot * a.spp + k;
-            acc[0] = acc[0] + s.Lr[p];
-            acc[1] = acc[1] + s.Lg[p];
-            acc[2] = acc[2] + s.Lb[p];
+        for (int32_t k0 = 0; k0 < a.spp; k0 += per_batch) {
+            const int32_t k1 = min(a.spp, k0 + per_batch);
+            const int64_t p0 = slot * a.spp + k0;
+            double b[3] = {s.Lr[p0], s.Lg[p0], s.Lb[p0]};
+            for (int32_t k = k0 + 1; k < k1; ++k) {
+                const int64_t p = slot * a.spp + k;
+                b[0] = b[0] + s.Lr[p];
+                b[1] = b[1] + s.Lg[p];
+                b[2] = b[2] + s.Lb[p];
+            }
+            acc[0] = acc[0] + b[0];
+            acc[1] = acc[1] + b[1];
+            acc[2] = acc[2] + b[2];
         }
         // (out_by_pixel: a raster frame, possibly rank 0's mapped over NVLink - the
         // frame "gather" is these stores, issued as each chunk's pixels finish)
-        const int64_t oi = (a.tiled || a.out_by_pixel) ? slot_pixel(a, slot) : a.out_offset + slot;
+        const int64_t oi = (a.tiled || a.out_by_pixel) ? pix : a.out_offset + slot;
         HRT_ASSERT(oi >= 0 && (!(a.tiled || a.out_by_pixel) || oi < (int64_t)a.cam.width * a.cam.height),
                    "output pixel", oi, (int64_t)a.cam.width * a.cam.height);
         double* o = a.out + 3 * oi;

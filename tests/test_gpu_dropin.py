@@ -74,3 +74,28 @@ def test_two_room_preset_with_shadows(ref, tmp_path, cuda):
     assert want.pixels.mean() > 0.01
     # finalize: the same PPM / PFM bytes as the reference's
     assert hrt.finalize(got, False) == ref["render"].finalize(want, False)
+
+
+def test_wide_frame_sums_group_like_the_reference(ref, cuda):
+    """512 x 20 at 12 spp: the reference sums each 16-row band's samples in
+    batches of 65536 // (16 * 512) = 8 (then 4; the 4-row last band in one
+    batch of 12, render.py:339-349); the GPU accumulate groups them the same
+    way, so the float64 image is bit-equal (a plain sample-order sum differs
+    in the last bits of ~2 % of the values)."""
+    import math
+    core, rr = ref["core"], ref["render"]
+    rf = importlib.import_module("hybridrt.field")
+    sf = importlib.import_module("hybridrt.surface")
+    g = np.random.default_rng(11)
+    field = rf.RadianceGrid((-1, -1, -1), (1, 1, 1), g.uniform(0, 1.5, (6, 6, 6)), g.uniform(0, 1, (6, 6, 6, 3)))
+    v, f = ref["assets"].quad((-3, -3, -1.5), (6, 0, 0.5), (0, 6, 0))
+    meshes = [sf.TriangleMesh(v, f, sf.Mirror(np.full(3, 0.8)))]
+    cam = rr.Camera(core.Transform.look_at((0, 0, 3), (0, 0, 0)), math.radians(30), (512, 20))
+    bvh = sf.Bvh(meshes)
+    scene = ref["scene"].Scene(config=None, camera=cam,
+                               render=ref["scene"].RenderConfig(spp=12, n_bounces=2, march_step=0.08, seed=4),
+                               field=field, meshes=meshes, bvh=bvh, blocker_bvh=bvh, emitters=None,
+                               collider_sdfs=[], spawn_eps=1e-4 * ref["scene"].scene_diagonal(field, meshes))
+    got = hrt.render(scene)
+    want = rr.render(scene)
+    assert np.array_equal(got.pixels, want.pixels)

@@ -133,3 +133,33 @@ def test_random_hybrid_scenes_bit_equal(hybridrt, seed):
     want = render(scene).pixels
     got = tracer.render(pack_scene(scene), pack_camera(cam), 4, seed)
     assert np.array_equal(got, want)
+
+
+def wide_frame_scene(h):
+    """A frame wide enough that the reference traces a 16-row band in several
+    batches of samples per pixel (render.py:339-349: 65536 // (16 * 512) = 8
+    samples per batch at w = 512; the last band of 4 rows takes 32): a
+    random dense grid in front of a tilted mirror quad."""
+    from hybridrt.assets import quad
+    from hybridrt.core import Transform
+    from hybridrt.field import RadianceGrid
+    from hybridrt.render import Camera
+    from hybridrt.surface import Mirror, TriangleMesh
+    g = np.random.default_rng(11)
+    field = RadianceGrid((-1, -1, -1), (1, 1, 1), g.uniform(0, 1.5, (6, 6, 6)), g.uniform(0, 1, (6, 6, 6, 3)))
+    v, f = quad((-3, -3, -1.5), (6, 0, 0.5), (0, 6, 0))
+    cam = Camera(Transform.look_at((0, 0, 3), (0, 0, 0)), math.radians(30), (512, 20))
+    return _ref_scene(h, field=field, meshes=[TriangleMesh(v, f, Mirror(np.full(3, 0.8)))], camera=cam,
+                      spp=12, n_bounces=2, march_step=0.08, seed=4)
+
+
+def test_render_batches_like_the_reference_on_wide_frames(hybridrt):
+    """Per-pixel sums grouped as the reference's sample batches: bit-equal
+    on a 512-wide frame at 12 spp (batches of 8 + 4 in full bands, 12 in
+    the 4-row last band), where a plain sample-order sum differs in the
+    last bits."""
+    from hybridrt.render import render
+    scene = wide_frame_scene(hybridrt)
+    want = render(scene).pixels
+    got = tracer.render(pack_scene(scene), pack_camera(scene.camera), 12, 4)
+    assert np.array_equal(got, want)
