@@ -632,7 +632,15 @@ def run_ours(args, rank, world, local):
     wl.r.render_pixels(wl.camera(args.warmup), wl.spp, 0, pixels=pix, out=out[:n_local])
     stages = {k: round(v, 3) for k, v in wl.r.last_stats["stage_ms"].items()}
     stage_frame_ms = wl.r.last_stats["ms"]
+    rrows, rms = wl.r.round_rows()                     # per march round: batch rows, engine ms
     wl.r.set_profile(False)
+    big = np.argsort(rrows)[::-1][:4] if len(rrows) else []
+    rounds_block = {
+        "rounds": int((rrows > 0).sum()), "batch_rows": int(rrows.sum()),
+        "engine_G_rows_per_s": float(rrows.sum() / (rms.sum() * 1e-3) / 1e9) if len(rrows) else None,
+        "largest_rounds_G_rows_per_s": [round(float(rrows[i] / (rms[i] * 1e-3) / 1e9), 2) for i in big],
+        "note": "hrt_round_rows of the profiled frame; the first (largest) rounds of a chunk carry the coherent "
+                "primary rays, the later ones the incoherent bounces (DESIGN 4.1)"}
     gather_gbs = wl.r.gather_peak(2)
     l2 = wl.r.l2_peak()
 
@@ -723,6 +731,7 @@ def run_ours(args, rank, world, local):
             "clocks": clk,
             "stages_ms": {"frame_ms": stage_frame_ms, **stages,
                           "note": "one untimed frame with hrt_set_profile (event pair per launch)"},
+            "field_rounds": rounds_block,
         }
         if extra:
             line["cfg1"] = extra

@@ -232,6 +232,8 @@ enum Counter { C_Q0 = 0, C_Q1 = 1, C_FETCH = 2,
                C_SHQ = 17, C_SHF = 18,
                // k_step in tail mode (G lanes per path) this round
                C_TAIL = 19,
+               // march-round ordinal of this render call (k_round_begin; hrt_round_rows)
+               C_RIDX = 20,
                C_COUNT = 16 };
 
 HRT_DEV d3 field_point(const DevField& f, d3 p) {

@@ -162,7 +162,7 @@ template <int E, int F>
 __global__ void __launch_bounds__(kThreads, 1)
 k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t n,
            const float4* __restrict__ dir32, float4* __restrict__ out, int32_t density_only,
-           const int32_t* __restrict__ round_ctr, unsigned long long* stats) {
+           const int32_t* __restrict__ round_ctr, unsigned long long* stats, int64_t* round_log) {
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr SmemPlan P = plan(E);
     constexpr nerf::WOff W = nerf::woff(E);
@@ -175,7 +175,11 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
     if (round_ctr) {                 // device-driven march round (kern::k_round_begin counters)
         set_rows(rmap, round_ctr[C_MQ0 + (round_ctr[C_CUR] ^ 1)], round_ctr[C_STRIDE]);
         n = (int64_t)rmap.width * round_ctr[C_S];
-        if (blockIdx.x == 0 && threadIdx.x == 0 && stats) atomicAdd(stats + S_ROWS, (unsigned long long)n);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            if (stats) atomicAdd(stats + S_ROWS, (unsigned long long)n);
+            const int32_t ri = round_ctr[C_RIDX] - 1;                  // (k_round_begin's ordinal)
+            if (round_log && ri >= 0 && ri < 1024) round_log[ri] = n;  // hrt_round_rows
+        }
     }
     if (n <= 0) return;              // empty round: skip the prologue
     const int64_t tiles = (n + kRows - 1) / kRows;

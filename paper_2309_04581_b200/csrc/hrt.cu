@@ -113,6 +113,8 @@ struct hrt_handle {
     int64_t trace_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t mev[2 * 1024] = {};
+    int64_t* round_rows = nullptr;  // device: batch rows of each device-driven march round (k_round_begin)
+    int32_t n_round_rows = 0;       // rounds logged by the last render call
     kern::MarchState ms{};
     int64_t batch_cap = 0;
     int32_t* pinned = nullptr;
@@ -676,7 +678,8 @@ int launch_ws(hrt_handle* h, const fws::SampleIn* in, fws::RowMap rm, int64_t n,
     const int grid = round_ctr ? h->sm_count
                                : (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)h->sm_count));
     fws::k_field_ws<E, F><<<grid, fws::kThreads, smem, st>>>(h->sc.field.nf, in, rm, n, dir32, out,
-                                                             density_only, round_ctr, h->ps.stats);
+                                                             density_only, round_ctr, h->ps.stats,
+                                                             round_ctr ? h->round_rows : nullptr);
     CK(cudaGetLastError());
     return HRT_OK;
 }
@@ -995,7 +998,8 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
         while (true) {
             for (int k = 0; k < kRoundsPerCheck; ++k) {
                 pbeg(h, st, HRT_STAGE_COMPOSITE);
-                kern::k_round_begin<<<1, 1, 0, st>>>(h->ps.counters, h->ps.stats, target, cap);
+                kern::k_round_begin<<<1, 1, 0, st>>>(h->ps.counters, h->ps.stats, target, cap,
+                                                    h->round_rows, kTimedLaunches);
                 if (a.mixed) kern::k_step<true><<<gs, kStepThreads, 0, st>>>(a, h->ms);
                 else kern::k_step<false><<<gs, kStepThreads, 0, st>>>(a, h->ms);
                 CK(cudaGetLastError());
@@ -1217,6 +1221,7 @@ int hrt_create(const hrt_scene_desc* d, hrt_handle** out) {
     if (d->field.kind == HRT_FIELD_NEURAL && !d->field.occ_bits) {
         if ((rc = build_occupancy(h, d->field.occ_threshold))) return bail(rc);
     }
+    if ((rc = h->alloc((size_t)kTimedLaunches * 8, reinterpret_cast<void**>(&h->round_rows)))) return bail(rc);
     CK(cudaDeviceSynchronize());
     *out = h;
     return HRT_OK;
@@ -1354,6 +1359,7 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
         stats->launches = h->launches;
         for (int i = 0; i < 8; ++i) stats->stage_ms[i] = (float)h->stage_ms[i];
         stats->batch_rows = h->batch_rows + (int64_t)tot[S_ROWS];
+        h->n_round_rows = std::min<int32_t>(ctr[C_RIDX], kTimedLaunches);
 #ifdef HRT_COUNT_STEPS
         fprintf(stderr, "shadow trace: node steps %llu  triangle tests %llu  blocked %llu  queued %s\n",
                 tot[5], tot[6], tot[7], "");
@@ -1790,6 +1796,24 @@ int hrt_gather_peak(hrt_handle* h, int32_t mode, double* gbs) {
     cudaEventDestroy(e1);
     cudaStreamDestroy(s2);
     cudaFree(sink);
+    return HRT_OK;
+}
+
+int hrt_round_rows(hrt_handle* h, int64_t* rows, float* field_ms, int32_t cap, int32_t* n) {
+    if (!h || !n) return fail(HRT_EINVAL, "null argument");
+    // device-driven rounds of the last hrt_render: round i launched the render's i-th
+    // field-engine pass (timed by the mev events in launch order)
+    const int32_t m = std::min(h->n_round_rows, std::min(cap, h->n_timed));
+    *n = m;
+    if (m <= 0) return HRT_OK;
+    if (rows) CK(cudaMemcpy(rows, h->round_rows, (size_t)m * 8, cudaMemcpyDeviceToHost));
+    if (field_ms) {
+        for (int32_t i = 0; i < m; ++i) {
+            float x = 0.f;
+            cudaEventElapsedTime(&x, h->mev[2 * i], h->mev[2 * i + 1]);
+            field_ms[i] = x;
+        }
+    }
     return HRT_OK;
 }
 

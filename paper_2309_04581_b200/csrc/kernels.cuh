@@ -1170,7 +1170,7 @@ __global__ void __launch_bounds__(256, HRT_SHTRACE_MINB) k_shadow_trace(Args a, 
 // read, fix its samples per path (kRoundSamples, more for small tail rounds,
 // capped by the batch buffer) and the batch strides, empty the next queue.
 __global__ void k_round_begin(int32_t* c, unsigned long long* stats, int32_t target_rows,
-                              int32_t batch_cap) {
+                              int32_t batch_cap, int64_t* round_rows, int32_t log_cap) {
     const int32_t cur = c[C_CUR] ^ 1;
     c[C_CUR] = cur;
     c[C_FIRST] = c[C_FIRST] == 2 ? 1 : 0;       // 2 = set by k_march_begin
@@ -1183,6 +1183,10 @@ __global__ void k_round_begin(int32_t* c, unsigned long long* stats, int32_t tar
         S = max(1, min(S, batch_cap / live));
     }
     c[C_S] = S;
+    if (round_rows) {                            // round ordinal for the engine's per-round row log
+        const int32_t ri = c[C_RIDX]++;
+        if (ri < log_cap) round_rows[ri] = 0;    // (empty rounds stay 0: round i = the i-th engine launch)
+    }
     c[C_TAIL] = live > 0 && live < kTailLive;
     c[C_PSTRIDE] = c[C_STRIDE];
     c[C_STRIDE] = live;

@@ -234,6 +234,17 @@ class Renderer:
         _lib.check(self.lib.hrt_gather_peak(self.handle, int(mode), ctypes.byref(v)), "hrt_gather_peak")
         return v.value
 
+    def round_rows(self, cap=1024):
+        """(rows, field_ms) per device-driven march round of the last render
+        (hrt_round_rows): batch rows (holes included) and field-engine time."""
+        rows = np.zeros(cap, np.int64)
+        ms = np.zeros(cap, np.float32)
+        n = ctypes.c_int32(0)
+        _lib.check(self.lib.hrt_round_rows(self.handle, rows.ctypes.data_as(ctypes.c_void_p),
+                                           ms.ctypes.data_as(ctypes.c_void_p), cap, ctypes.byref(n)),
+                   "hrt_round_rows")
+        return rows[:n.value], ms[:n.value]
+
     def l2_peak(self):
         """Measured L2 roofline over this scene's hash table (hrt_l2_peak):
         coalesced read GB/s and random 32-B sector-gather GB/s."""
