@@ -15,6 +15,7 @@ from .images import HdrImage, decode_pfm, decode_ppm, encode_pfm, encode_ppm
 from .scene import Camera, EmitterSet, RenderConfig, Scene, make_scene, scene_diagonal
 from .surface import Dielectric, Lambertian, Mirror, TriangleMesh
 from .rng import PathRng
+from .nerffile import load_nerf, load_scene, save_nerf
 
 _RENDER_NAMES = ("render", "render_surface_only", "render_volume_only", "trace_path", "finalize",
                  "Renderer", "renderer_for")
@@ -32,4 +33,4 @@ def __getattr__(name):
 __all__ = ["Ray", "Transform", "tone_map", "NeuralField", "RadianceGrid", "HdrImage",
            "decode_pfm", "decode_ppm", "encode_pfm", "encode_ppm", "Camera", "EmitterSet",
            "RenderConfig", "Scene", "make_scene", "scene_diagonal", "Dielectric", "Lambertian",
-           "Mirror", "TriangleMesh", "PathRng", *_RENDER_NAMES]
+           "Mirror", "TriangleMesh", "PathRng", "load_nerf", "load_scene", "save_nerf", *_RENDER_NAMES]

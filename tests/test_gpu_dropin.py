@@ -103,3 +103,39 @@ def test_wide_frame_sums_group_like_the_reference(ref, cuda):
     d = np.abs(got.pixels - want.pixels)
     assert d.max() < 1e-12, d.max()
     assert np.mean(d == 0.0) > 0.5
+
+
+def test_nerf_scene_from_the_reference_json(ref, tmp_path, cuda):
+    """A NeRF scene loaded from disk through the reference's scene JSON
+    (`hrt.load_scene`: its parser / builder, the `.hrtnerf` field file with
+    the hyper-parameters in its header) renders bit-identically to the same
+    scene built in memory, and matches the oracle."""
+    import json
+    import math
+    from oracle import tracer
+    from paper_2309_04581_b200 import Camera, Mirror, RenderConfig, Scene, TriangleMesh, assets, configs
+    from paper_2309_04581_b200.pack import pack_camera
+    field = configs.network(0)
+    hrt.save_nerf(tmp_path / "fog.hrtnerf", field)
+    v, f = assets.icosphere(0.4, 2)
+    ref["scene"]  # (reference importable: the loader uses its parser)
+    importlib.import_module("hybridrt.surface").save_obj(str(tmp_path / "ball.obj"), v, f)
+    doc = {"field": {"path": "fog.hrtnerf"},
+           "meshes": [{"path": "ball.obj", "bsdf": {"type": "mirror", "reflectance": [1.0, 1.0, 1.0]}}],
+           "camera": {"position": [0.0, 0.0, 3.0], "look_at": [0.0, 0.0, 0.0], "up": [0.0, 1.0, 0.0],
+                      "fov_deg": 40.0, "resolution": [48, 48]},
+           "render": {"spp": 1, "n_bounces": 2, "march_step": configs.MARCH_STEP, "seed": 0}}
+    (tmp_path / "scene.json").write_text(json.dumps(doc))
+    scene = hrt.load_scene(str(tmp_path / "scene.json"))
+    got = hrt.render(scene)
+    assert type(got) is ref["images"].HdrImage
+    mem = Scene(camera=Camera(hrt.Transform.look_at((0, 0, 3), (0, 0, 0)), math.radians(40.0), (48, 48)),
+                render=RenderConfig(spp=1, n_bounces=2, march_step=configs.MARCH_STEP, seed=0),
+                field=field, meshes=[TriangleMesh(scene.meshes[0].vertices, scene.meshes[0].indices,
+                                                  Mirror(np.ones(3)))])      # (the OBJ text round trip)
+    assert mem.spawn_eps == scene.spawn_eps
+    want = hrt.render(mem)
+    assert np.array_equal(got.pixels, want.pixels)
+    r = scene._hrt_renderer.r
+    oracle = tracer.render(r.pack, pack_camera(scene.camera), 1, 0)
+    assert np.abs(got.pixels - oracle).max() < 1e-3

@@ -172,3 +172,49 @@ def test_renderer_cache_tracks_bvh_object_and_field_placement(hybridrt):
     assert not c.geometry_changed(scene)
     scene.field.world_from_field = core.Transform.translate((0.1, 0.0, 0.0))
     assert _field_key(scene) != c.field and not c.geometry_changed(scene)
+
+
+def test_nerf_file_round_trip(tmp_path):
+    """.hrtnerf: hyper-parameters in the header, arrays bit-exact."""
+    from paper_2309_04581_b200.nerffile import is_nerf_file, load_nerf, save_nerf
+    f = NeuralField.random(5, n_levels=8, n_features=2, log2_table=12, n_min=16, n_max=128,
+                           out_activation="softplus", occupancy_res=32)
+    f.world_from_field = Transform.translate((0.25, -0.5, 0.0))
+    p = tmp_path / "f.hrtnerf"
+    save_nerf(p, f)
+    assert is_nerf_file(p) and not is_nerf_file(__file__)
+    g = load_nerf(p)
+    for name in ("table", "w_density1", "w_density2", "w_color1", "w_color2", "w_color3"):
+        a, b = getattr(f, name), getattr(g, name)
+        assert a.dtype == b.dtype and np.array_equal(a, b), name
+    assert (g.n_levels, g.n_features, g.log2_table, g.n_min, g.n_max) == (8, 2, 12, 16, 128)
+    assert g.out_activation == "softplus" and g.occupancy_res == 32
+    assert np.array_equal(g.world_from_field.m, f.world_from_field.m)
+    assert np.array_equal(g.bbox_lo, f.bbox_lo) and np.array_equal(g.bbox_hi, f.bbox_hi)
+
+
+def test_load_scene_with_a_nerf_field_file(hybridrt, tmp_path):
+    """A reference scene JSON whose field.path is a .hrtnerf file loads
+    through the reference's own parser / builder with the NeuralField
+    attached (the hyper-parameters live in the field file)."""
+    import json as _json
+    import importlib
+    from paper_2309_04581_b200 import assets
+    from paper_2309_04581_b200.nerffile import load_scene, save_nerf
+    f = NeuralField.random(3, n_levels=8, n_features=2, log2_table=12, n_min=16, n_max=128)
+    save_nerf(tmp_path / "fog.hrtnerf", f)
+    v, fc = assets.icosphere(0.4, 2)
+    importlib.import_module("hybridrt.surface").save_obj(str(tmp_path / "ball.obj"), v, fc)
+    doc = {"field": {"path": "fog.hrtnerf", "transform": {"translate": [0.0, 0.1, 0.0]}},
+           "meshes": [{"path": "ball.obj", "bsdf": {"type": "mirror", "reflectance": [1.0, 1.0, 1.0]}}],
+           "camera": {"position": [0.0, 0.0, 3.0], "look_at": [0.0, 0.0, 0.0], "up": [0.0, 1.0, 0.0],
+                      "fov_deg": 40.0, "resolution": [16, 16]},
+           "render": {"spp": 1, "n_bounces": 2, "march_step": 0.0203, "seed": 0}}
+    (tmp_path / "s.json").write_text(_json.dumps(doc))
+    scene = load_scene(str(tmp_path / "s.json"))
+    assert type(scene).__module__.startswith("hybridrt")
+    assert scene.field.kind == "neural" and np.array_equal(scene.field.table, f.table)
+    assert scene.field.world_from_field.m[1, 3] == 0.1
+    assert len(scene.meshes) == 1 and scene.spawn_eps > 0
+    pk = pack_scene(scene)
+    assert pk["field"]["kind"] == 2 and not pk["field"]["identity"]
