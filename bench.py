@@ -632,7 +632,7 @@ def run_ours(args, rank, world, local):
     wl.r.render_pixels(wl.camera(args.warmup), wl.spp, 0, pixels=pix, out=out[:n_local])
     stages = {k: round(v, 3) for k, v in wl.r.last_stats["stage_ms"].items()}
     stage_frame_ms = wl.r.last_stats["ms"]
-    rrows, rms = wl.r.round_rows()                     # per march round: batch rows, engine ms
+    rrows, _, rms = wl.r.round_rows()                  # per march round: batch rows, engine ms
     wl.r.set_profile(False)
     big = np.argsort(rrows)[::-1][:4] if len(rrows) else []
     rounds_block = {

@@ -254,9 +254,11 @@ int hrt_set_field_transform(hrt_handle* h, int32_t identity, const double* field
 
 /* Measurement: for the last hrt_render's device-driven march rounds (neural
  * field, continuous march), the batch rows of each round (live paths x
- * samples per path, holes included) and the field-engine launch time of that
- * round (ms, CUDA events); *n = rounds reported (<= cap). */
-int hrt_round_rows(hrt_handle* h, int64_t* rows, float* field_ms, int32_t cap, int32_t* n);
+ * samples per path, holes included), the samples generated into them, and
+ * the field-engine launch time of that round (ms, CUDA events); *n = rounds
+ * reported (<= cap). Any output pointer may be NULL. */
+int hrt_round_rows(hrt_handle* h, int64_t* rows, int64_t* samples, float* field_ms, int32_t cap,
+                   int32_t* n);
 
 /* L2 roofline probe (bench.py "roofline"): GB/s of coalesced 16-B reads of
  * this scene's hash table while it is L2-resident (all SMs, 8 passes), and

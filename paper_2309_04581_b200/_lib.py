@@ -120,7 +120,7 @@ SIGNATURES = {
     "hrt_ipc_close": (ctypes.c_int, [vp]),
     "hrt_gather_peak": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
     "hrt_set_field_transform": (ctypes.c_int, [vp, ctypes.c_int32, vp]),
-    "hrt_round_rows": (ctypes.c_int, [vp, vp, vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]),
+    "hrt_round_rows": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]),
     "hrt_l2_peak": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                    ctypes.POINTER(ctypes.c_int64)]),
     "hrt_refit": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),

@@ -1221,7 +1221,7 @@ int hrt_create(const hrt_scene_desc* d, hrt_handle** out) {
     if (d->field.kind == HRT_FIELD_NEURAL && !d->field.occ_bits) {
         if ((rc = build_occupancy(h, d->field.occ_threshold))) return bail(rc);
     }
-    if ((rc = h->alloc((size_t)kTimedLaunches * 8, reinterpret_cast<void**>(&h->round_rows)))) return bail(rc);
+    if ((rc = h->alloc((size_t)kTimedLaunches * 16, reinterpret_cast<void**>(&h->round_rows)))) return bail(rc);
     CK(cudaDeviceSynchronize());
     *out = h;
     return HRT_OK;
@@ -1799,7 +1799,7 @@ int hrt_gather_peak(hrt_handle* h, int32_t mode, double* gbs) {
     return HRT_OK;
 }
 
-int hrt_round_rows(hrt_handle* h, int64_t* rows, float* field_ms, int32_t cap, int32_t* n) {
+int hrt_round_rows(hrt_handle* h, int64_t* rows, int64_t* samples, float* field_ms, int32_t cap, int32_t* n) {
     if (!h || !n) return fail(HRT_EINVAL, "null argument");
     // device-driven rounds of the last hrt_render: round i launched the render's i-th
     // field-engine pass (timed by the mev events in launch order)
@@ -1807,6 +1807,14 @@ int hrt_round_rows(hrt_handle* h, int64_t* rows, float* field_ms, int32_t cap, i
     *n = m;
     if (m <= 0) return HRT_OK;
     if (rows) CK(cudaMemcpy(rows, h->round_rows, (size_t)m * 8, cudaMemcpyDeviceToHost));
+    if (samples) {               // cumulative snapshots at each round's start -> per-round counts
+        std::vector<int64_t> snap(m);
+        CK(cudaMemcpy(snap.data(), h->round_rows + kTimedLaunches, (size_t)m * 8, cudaMemcpyDeviceToHost));
+        unsigned long long tot[S_COUNT];
+        CK(cudaMemcpy(tot, h->ps.stats, sizeof(tot), cudaMemcpyDeviceToHost));
+        for (int32_t i = 0; i < m; ++i)
+            samples[i] = (i + 1 < m ? snap[i + 1] : (int64_t)tot[S_EVALS]) - snap[i];
+    }
     if (field_ms) {
         for (int32_t i = 0; i < m; ++i) {
             float x = 0.f;

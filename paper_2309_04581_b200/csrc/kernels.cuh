@@ -1185,7 +1185,10 @@ __global__ void k_round_begin(int32_t* c, unsigned long long* stats, int32_t tar
     c[C_S] = S;
     if (round_rows) {                            // round ordinal for the engine's per-round row log
         const int32_t ri = c[C_RIDX]++;
-        if (ri < log_cap) round_rows[ri] = 0;    // (empty rounds stay 0: round i = the i-th engine launch)
+        if (ri < log_cap) {
+            round_rows[ri] = 0;                  // (empty rounds stay 0: round i = the i-th engine launch)
+            round_rows[log_cap + ri] = (int64_t)stats[S_EVALS];   // samples generated before round i
+        }
     }
     c[C_TAIL] = live > 0 && live < kTailLive;
     c[C_PSTRIDE] = c[C_STRIDE];

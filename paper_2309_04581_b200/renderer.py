@@ -235,15 +235,18 @@ class Renderer:
         return v.value
 
     def round_rows(self, cap=1024):
-        """(rows, field_ms) per device-driven march round of the last render
-        (hrt_round_rows): batch rows (holes included) and field-engine time."""
+        """(rows, samples, field_ms) per device-driven march round of the last
+        render (hrt_round_rows): batch rows (holes included), the samples in
+        them, and the field-engine time."""
         rows = np.zeros(cap, np.int64)
+        smp = np.zeros(cap, np.int64)
         ms = np.zeros(cap, np.float32)
         n = ctypes.c_int32(0)
         _lib.check(self.lib.hrt_round_rows(self.handle, rows.ctypes.data_as(ctypes.c_void_p),
+                                           smp.ctypes.data_as(ctypes.c_void_p),
                                            ms.ctypes.data_as(ctypes.c_void_p), cap, ctypes.byref(n)),
                    "hrt_round_rows")
-        return rows[:n.value], ms[:n.value]
+        return rows[:n.value], smp[:n.value], ms[:n.value]
 
     def l2_peak(self):
         """Measured L2 roofline over this scene's hash table (hrt_l2_peak):

@@ -21,12 +21,12 @@ r.render_pixels(scene.camera, spp, 0)
 torch.cuda.synchronize()
 r.render_pixels(scene.camera, spp, 0)
 st = r.last_stats
-rows, ms = r.round_rows()
+rows, smp, ms = r.round_rows()
 live = rows > 0
 out = {"cfg": cfg, "frame_ms": st["ms"], "field_ms": st["field_ms"], "samples": st["nerf_samples"],
        "batch_rows": int(rows.sum()), "rounds": int(live.sum()),
        "rows_per_s_frame": float(rows.sum() / (ms.sum() * 1e-3)),
-       "per_round": [{"i": i, "rows": int(rows[i]), "ms": round(float(ms[i]), 4),
+       "per_round": [{"i": i, "rows": int(rows[i]), "samples": int(smp[i]), "ms": round(float(ms[i]), 4),
                       "G_rows_per_s": round(float(rows[i] / (ms[i] * 1e-3) / 1e9), 3) if ms[i] > 0 else None}
                      for i in range(len(rows)) if rows[i] > 0]}
 print(json.dumps(out))
