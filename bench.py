@@ -632,15 +632,16 @@ def run_ours(args, rank, world, local):
     wl.r.render_pixels(wl.camera(args.warmup), wl.spp, 0, pixels=pix, out=out[:n_local])
     stages = {k: round(v, 3) for k, v in wl.r.last_stats["stage_ms"].items()}
     stage_frame_ms = wl.r.last_stats["ms"]
-    rrows, _, rms = wl.r.round_rows()                  # per march round: batch rows, engine ms
+    rrows, rsmp, rms = wl.r.round_rows()               # per march round: batch rows, samples, engine ms
     wl.r.set_profile(False)
-    big = np.argsort(rrows)[::-1][:4] if len(rrows) else []
+    live = rrows > 0
     rounds_block = {
-        "rounds": int((rrows > 0).sum()), "batch_rows": int(rrows.sum()),
-        "engine_G_rows_per_s": float(rrows.sum() / (rms.sum() * 1e-3) / 1e9) if len(rrows) else None,
-        "largest_rounds_G_rows_per_s": [round(float(rrows[i] / (rms[i] * 1e-3) / 1e9), 2) for i in big],
-        "note": "hrt_round_rows of the profiled frame; the first (largest) rounds of a chunk carry the coherent "
-                "primary rays, the later ones the incoherent bounces (DESIGN 4.1)"}
+        "rounds": int(live.sum()), "batch_rows": int(rrows.sum()), "samples": int(rsmp.sum()),
+        "hole_fraction": float(1.0 - rsmp.sum() / max(1, rrows.sum())),
+        "first_rounds_G_samples_per_s": [round(float(rsmp[i] / (rms[i] * 1e-3) / 1e9), 2)
+                                         for i in np.nonzero(live)[0][:8]],
+        "note": "hrt_round_rows of the profiled frame (first chunk's rounds): the first rounds carry the "
+                "coherent primary rays, the later ones the incoherent bounces (DESIGN 4.1)"}
     gather_gbs = wl.r.gather_peak(2)
     l2 = wl.r.l2_peak()
 
