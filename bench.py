@@ -358,7 +358,7 @@ def shipped_block(workers):
 def cpu_baseline_block(config, n_tiles=0):
     workers = cpu_workers()
     (w, h), spp = _frame_shape(config)
-    n_tiles = n_tiles or (2 * workers if config == "cfg3" else max(16, 8 * workers))
+    n_tiles = n_tiles or (4 * workers if config == "cfg3" else max(16, 8 * workers))   # ~10 s on 16 cores
     pool = cpu_pool(config, workers)
     samples, paths, dt = cpu_sample(config, n_tiles, pool)
     pool.close()
