@@ -50,6 +50,9 @@ WORKLOADS = {
             "L16 F2 T2^19 16->2048 hash-grid NeRF (seed 1), 1920x1080, 8 spp, 4 bounces, 128^3 "
             "occupancy, 1024-sample cap, early-out 1e-4; each step = GPU rigid refit of the next of "
             "30 seeded motion frames + the full frame",
+    "cfg4": "cfg4: emissive quad (radiance 10, r_src 1) + shadow rays occluded by a 300k-triangle displaced "
+            "torus in the L16 F4 T2^21 16->4096 softplus HDR NeRF (seed 4), 3840x2160, 64 spp (8x8 stratified), "
+            "6 bounces; each step = one full 4K frame",
     "cfg1": "cfg1: glass icosphere s5 (20480 tris, IOR 1.5) in L16 F2 T2^19 16->2048 hash-grid NeRF, "
             "800x800, 1 spp, 4 bounces, 128^3 occupancy, 1024-sample cap, early-out 1e-4, 100 seeded "
             "cameras (step k = camera k mod 100)",
@@ -63,7 +66,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["cfg3", "cfg1"], default="cfg3")
+    ap.add_argument("--config", choices=["cfg3", "cfg1", "cfg4"], default="cfg3")
     ap.add_argument("--cpu-tiles", type=int, default=0,
                     help="16x16 tiles per CPU sample (0 = scaled to the worker count)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -202,7 +205,7 @@ def _cpu_scene(config):
         from oracle import tracer
         from paper_2309_04581_b200 import configs
         from paper_2309_04581_b200.pack import pack_camera, pack_scene
-        scene = configs.cfg3() if config == "cfg3" else configs.cfg1()
+        scene = {"cfg3": configs.cfg3, "cfg1": configs.cfg1, "cfg4": configs.cfg4}[config]()
         _CPU[config] = (tracer.OracleScene(pack_scene(scene)), pack_camera(scene.camera))
     return _CPU[config]
 
@@ -279,7 +282,11 @@ def cpu_pool(config, workers):
 
 
 def _frame_shape(config):
-    return ((1920, 1080), 8) if config == "cfg3" else ((800, 800), 1)
+    return {"cfg3": ((1920, 1080), 8), "cfg1": ((800, 800), 1), "cfg4": ((3840, 2160), 64)}[config]
+
+
+def _cpu_tile_size(config):
+    return 8 if config == "cfg4" else TILE          # (a 16x16 x 64 spp cfg4 tile is minutes of CPU)
 
 
 def cpu_sample(config, n_tiles, pool, cam_index=0, seed=0):
@@ -288,12 +295,13 @@ def cpu_sample(config, n_tiles, pool, cam_index=0, seed=0):
     import numpy as np
     (w, h), spp = _frame_shape(config)
     rng = np.random.default_rng(seed)
-    tx = w // TILE
-    chosen = rng.choice(tx * (h // TILE), n_tiles, replace=False)
+    ts = _cpu_tile_size(config)
+    tx = w // ts
+    chosen = rng.choice(tx * (h // ts), n_tiles, replace=False)
     jobs = []
     for t in chosen:
-        x0, y0 = (t % tx) * TILE, (t // tx) * TILE
-        ys, xs = np.meshgrid(np.arange(y0, y0 + TILE), np.arange(x0, x0 + TILE), indexing="ij")
+        x0, y0 = (t % tx) * ts, (t // tx) * ts
+        ys, xs = np.meshgrid(np.arange(y0, y0 + ts), np.arange(x0, x0 + ts), indexing="ij")
         jobs.append((config, cam_index, (ys * w + xs).reshape(-1), spp))
     t0 = time.perf_counter()
     res = pool.map(_cpu_tile, jobs, chunksize=1)
@@ -358,14 +366,14 @@ def shipped_block(workers):
 def cpu_baseline_block(config, n_tiles=0):
     workers = cpu_workers()
     (w, h), spp = _frame_shape(config)
-    n_tiles = n_tiles or (4 * workers if config == "cfg3" else max(16, 8 * workers))   # ~10 s on 16 cores
+    n_tiles = n_tiles or {"cfg3": 4 * workers, "cfg4": workers}.get(config, max(16, 8 * workers))  # ~10-30 s
     pool = cpu_pool(config, workers)
     samples, paths, dt = cpu_sample(config, n_tiles, pool)
     pool.close()
     pool.join()
     return {"value": samples / dt, "unit": "samples/s", "cores": workers, "kind": "port",
             "cpu": cpu_model(), "mrays_per_s": paths / dt / 1e6,
-            "sample": f"{n_tiles} seeded 16x16 x {spp} spp tiles ({paths} paths, {samples} NeRF samples) "
+            "sample": f"{n_tiles} seeded {_cpu_tile_size(config)}x{_cpu_tile_size(config)} x {spp} spp tiles ({paths} paths, {samples} NeRF samples) "
                       f"of the {config} frame-0 {w}x{h} frame, oracle/ numpy port of the reference "
                       f"render loop + neural field, one process per core, {dt:.1f} s wall",
             "reference_as_shipped": shipped_block(workers) if config == "cfg3" else None}
@@ -378,7 +386,7 @@ def run_reference(args, rank, world):
         return
     workers = cpu_workers()
     (w, h), spp = _frame_shape(args.config)
-    n_tiles = args.cpu_tiles or (workers if args.config == "cfg3" else max(8, 4 * workers))
+    n_tiles = args.cpu_tiles or {"cfg3": workers, "cfg4": workers // 2 or 1}.get(args.config, max(8, 4 * workers))
     pool = cpu_pool(args.config, workers)
     for _ in range(max(0, min(args.warmup, 1))):
         cpu_sample(args.config, max(1, workers), pool)
@@ -453,6 +461,12 @@ class Workload:
             self.xf = [Renderer.pinned((n, 3, 4), np.float64) for _ in range(CFG3_FRAMES)]
             for f in range(CFG3_FRAMES):
                 self.xf[f][:] = configs.cfg3_transforms(f)
+            self.cams = [self.scene.camera]
+            self.spp = self.scene.render.spp
+        elif config == "cfg4":
+            self.scene = configs.cfg4()
+            self.r = Renderer(self.scene)
+            self.xf = None
             self.cams = [self.scene.camera]
             self.spp = self.scene.render.spp
         else:
@@ -642,7 +656,7 @@ def run_ours(args, rank, world, local):
                                          for i in np.nonzero(live)[0][:8]],
         "note": "hrt_round_rows of the profiled frame (first chunk's rounds): the first rounds carry the "
                 "coherent primary rays, the later ones the incoherent bounces (DESIGN 4.1)"}
-    gather_gbs = wl.r.gather_peak(2)
+    gather_gbs = wl.r.gather_peak(2) if wl.field.n_features == 2 else None   # (8-B gather probe: F = 2)
     l2 = wl.r.l2_peak()
 
     extra = None
@@ -669,7 +683,10 @@ def run_ours(args, rank, world, local):
         traffic, traffic_src = ncu_traffic(args.config)
         traffic = traffic or {}
         req_per_sample = traffic.get("l2_requests_per_sample")
-        peak_requests = gather_gbs * 1e9 / 8.0                             # one request per random 8-B gather
+        peak_requests = gather_gbs * 1e9 / 8.0 if gather_gbs else None    # one request per random 8-B gather
+        table_bytes = l2["bytes"]
+        l2_resident = table_bytes < 96 * 2**20                              # the 126 MB L2 holds the table
+        roof_peak = l2["read_gbs"] if l2_resident else hbm
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
@@ -690,32 +707,35 @@ def run_ours(args, rank, world, local):
                        "refit_ms_per_step": rank0["refit_ms"] / args.steps},
             "gpu_launches": int(rank0["launches"]),
             "roofline": {
-                "bound": "l2", "kernel": "fws::k_field_ws<32,2> (warp-specialized hash encode + 5-layer "
-                                         "tcgen05 MLP, TMEM operands)",
-                "achieved": achieved, "peak": l2["read_gbs"], "unit": "GB/s",
-                "frac": achieved / l2["read_gbs"],
+                "bound": "l2" if l2_resident else "hbm",
+                "kernel": f"fws::k_field_ws<{field.enc_dim},{field.n_features}> (warp-specialized hash encode + "
+                          "5-layer tcgen05 MLP, TMEM operands)",
+                "achieved": achieved, "peak": roof_peak, "unit": "GB/s",
+                "frac": achieved / roof_peak,
                 "traffic": traffic.get("dram_bytes_per_launch"),
                 "l2_bytes_per_launch": traffic.get("l2_bytes_per_launch"),
                 "bytes_per_sample": enc_bytes, "launches": int(rank0["field_launches"]),
                 "avg_launch_ms": march_ms / max(1, rank0["field_launches"]),
-                "peak_source": "hrt_l2_peak (live, this run): coalesced 16-B reads of an L2-resident "
-                               f"{l2['bytes'] / 2**20:.1f} MiB buffer (the hash table's size) by every SM; "
-                               "achieved = algorithmic encode bytes (8 corners x L x F x 4 B) x field-engine "
+                "peak_source": ("hrt_l2_peak (live, this run): coalesced 16-B reads of the L2-resident "
+                                f"{table_bytes / 2**20:.1f} MiB hash table by every SM" if l2_resident else
+                                f"{peak_src} hbm_gbs (burst copy): the {table_bytes / 2**20:.0f} MiB table does "
+                                "not fit the 126 MB L2") +
+                               "; achieved = algorithmic encode bytes (8 corners x L x F x 4 B) x field-engine "
                                "samples/s; traffic = ncu dram bytes per field-engine launch (" +
                                (traffic_src or "no capture") + ")",
-                "hbm": {"peak": hbm, "frac": achieved / hbm, "source": peak_src + " hbm_gbs (burst copy); "
-                        "the 46.5 MiB table is L2-resident, so HBM is not the bound"},
+                "hbm": {"peak": hbm, "frac": achieved / hbm, "source": peak_src + " hbm_gbs (burst copy)"},
+                "l2_read_gbs": l2["read_gbs"],
             },
             "roofline_gather": {
                 "bound": "L1 miss requests to L2 (random gathers, ~1 request/clk/SM)",
                 "achieved": field_sps * req_per_sample if req_per_sample else None,
                 "peak": peak_requests, "unit": "requests/s",
-                "frac": field_sps * req_per_sample / peak_requests if req_per_sample else None,
+                "frac": field_sps * req_per_sample / peak_requests if req_per_sample and peak_requests else None,
                 "requests_per_sample": req_per_sample,
                 "sectors_per_sample": traffic.get("l2_sectors_per_sample"),
                 "random_sector_gbs": l2["gather_sector_gbs"],
                 "peak_source": "hrt_gather_peak (live, this run): independent random 8-B gathers over the "
-                               f"same table, {gather_gbs:.0f} GB/s useful = 1 request each; requests/sample from "
+                               f"same table, {gather_gbs or 0:.0f} GB/s useful = 1 request each; requests/sample from "
                                f"{traffic_src} (ncu lts__t_requests_srcunit_tex_op_read over every field-engine "
                                f"launch of one frame, commit {traffic.get('commit')})",
             },
