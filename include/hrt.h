@@ -261,9 +261,10 @@ int hrt_round_rows(hrt_handle* h, int64_t* rows, int64_t* samples, float* field_
                    int32_t* n);
 
 /* L2 roofline probe (bench.py "roofline"): GB/s of coalesced 16-B reads of
- * this scene's hash table while it is L2-resident (all SMs, 8 passes), and
- * GB/s of random whole 32-B sector gathers over it (lane pairs, L1
- * bypassed); *bytes = the table's size. Device-synchronous, default stream. */
+ * this scene's hash table (its first 64 MiB if larger) while it is
+ * L2-resident (all SMs, 8 passes), and GB/s of random whole 32-B sector
+ * gathers over it (lane pairs, L1 bypassed); *bytes = the probed size.
+ * Device-synchronous, default stream. */
 int hrt_l2_peak(hrt_handle* h, double* read_gbs, double* sector_gbs, int64_t* bytes);
 
 /* New world-space face geometry (same topology; host pointers). */

@@ -1843,7 +1843,9 @@ int hrt_l2_peak(hrt_handle* h, double* read_gbs, double* sector_gbs, int64_t* by
     if (!h || !read_gbs || !sector_gbs) return fail(HRT_EINVAL, "null argument");
     if (h->sc.field.kind != HRT_FIELD_NEURAL) return fail(HRT_EINVAL, "needs a neural field");
     const NeuralField& nf = h->sc.field.nf;
-    const int64_t nbytes = (int64_t)h->tab_entries * h->F * 4;
+    // (tables larger than 64 MiB - cfg4's 344 MiB - are probed over their first 64 MiB so the
+    // buffer stays L2-resident: the probe measures L2, not DRAM)
+    const int64_t nbytes = std::min<int64_t>((int64_t)h->tab_entries * h->F * 4, int64_t(64) << 20);
     const int64_t n16 = nbytes / 16;
     const uint4* buf = reinterpret_cast<const uint4*>(nf.table);
     float* sink = nullptr;
