@@ -57,6 +57,13 @@ __device__ unsigned long long ws_prof[8];
 #endif
 constexpr bool kSynthEncode = HRT_SYNTH_ENCODE;   // measurement build: MLP fed without gathers
 constexpr int kEncWarps = 16;               // 4 level quarters x 4 lane quarters
+// Encode teams (template T): with T = 2 the 16 encode warps form two teams
+// of 8 (2 level halves x 4 lane quarters, one level of gathers in flight per
+// thread) that take alternate tiles, so two tiles are in flight per SM.
+// Measured per round (DESIGN 4.2): +5-7 % on the first, L1-coherent march
+// rounds of a chunk, -1-3 % on the later incoherent ones, so the host runs
+// T = 2 for the first kTeamRounds rounds only. Same per-level arithmetic:
+// the features do not depend on T.
 constexpr int kInflight = HRT_WS_INFLIGHT;  // levels of gathers in flight per encode thread
 #ifndef HRT_WS_INFLIGHT4
 #define HRT_WS_INFLIGHT4 1
@@ -158,7 +165,7 @@ __device__ __forceinline__ void relu64_tmem(uint32_t accum, uint32_t act) {
 // Batch evaluation of n samples -> out[i] = (sigma, r, g, b).
 // dir32[path] is the field-frame unit direction; density_only skips the
 // colour head (rgb = 0).
-template <int E, int F>
+template <int E, int F, int T = 1>
 __global__ void __launch_bounds__(kThreads, 1)
 k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t n,
            const float4* __restrict__ dir32, float4* __restrict__ out, int32_t density_only,
@@ -167,7 +174,8 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
     constexpr SmemPlan P = plan(E);
     constexpr nerf::WOff W = nerf::woff(E);
     constexpr int L = E / F;
-    constexpr int NL = L / 4;                     // levels per encode thread
+    constexpr int LG = 4 / T;                     // level groups per team
+    constexpr int NL = L / LG;                    // levels per encode thread
     constexpr int NC = NL * F / 2;                // TMEM columns per encode thread
     constexpr uint32_t kStageCols = E / 2;
     constexpr int kStages = kStagesE<E>;
@@ -195,7 +203,7 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
     if (warp == kEncWarps + kMlpWarps) umma::tmem_alloc(umma::saddr(tslot), kTmemCols);
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
-            umma::mbar_init(bar_full(bars, s), kEncWarps * 32);
+            umma::mbar_init(bar_full(bars, s), kEncWarps / T * 32);   // one team fills a stage
             umma::mbar_init(bar_empty(bars, s), 1);
         }
         for (int g = 0; g < kMlpGroups; ++g) {
@@ -217,11 +225,13 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
         // (one code path for all level quarters: warps of all four quarters
         // share each scheduler, and four specialised copies of this loop
         // thrash the instruction cache - measured 1.9x slower)
-        const int q = warp >> 2;                    // level quarter
+        const int q = (warp >> 2) % LG;             // level group
+        const int team = (warp >> 2) / LG;
         const int r = (warp & 3) * 32 + (threadIdx.x & 31);   // row == TMEM lane
         const float3 lo = make_float3(nf.lo32[0], nf.lo32[1], nf.lo32[2]);
-        int it = 0;
-        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        int it = team;
+        for (int64_t t = blockIdx.x + (int64_t)team * gridDim.x; t < tiles;
+             t += (int64_t)T * gridDim.x, it += T) {
             const int s = it % kStages;
             const uint32_t ph = (uint32_t)((it / kStages) & 1);
             const int64_t l = t * kRows + r;
@@ -236,9 +246,9 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
                     // gathers - what the MLP pipeline sustains when it is fed
 #pragma unroll
                     for (int k = 0; k < NL * F; ++k) v[k] = 0.01f * (float)k * rel.x - rel.y;
-                } else if constexpr (NL % kInflightF<F> == 0) {
-                    // kInflightF levels of gathers in flight per thread
-                    constexpr int IF = kInflightF<F>;
+                } else if constexpr (NL % (T == 2 ? 1 : kInflightF<F>) == 0) {
+                    // kInflightF levels of gathers in flight per thread (1 with two teams)
+                    constexpr int IF = T == 2 ? 1 : kInflightF<F>;
 #pragma unroll
                     for (int j = 0; j < NL; j += IF) {
                         nerf::LevelLoadsF<F> g[IF];

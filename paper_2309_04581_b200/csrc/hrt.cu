@@ -59,6 +59,10 @@ constexpr int64_t kBatchCap = int64_t(1) << HRT_BATCH_CAP_LOG2;   // samples per
 #define HRT_TEX_LEVELS 8
 #endif
 constexpr int kTexLevels = HRT_TEX_LEVELS;        // finest levels gathered via TEX
+#ifndef HRT_TEAM_ROUNDS
+#define HRT_TEAM_ROUNDS 3
+#endif
+constexpr int kTeamRounds = HRT_TEAM_ROUNDS;       // march rounds run with two encode teams (fws T = 2)
 #ifndef HRT_MIXED_MARCH
 #define HRT_MIXED_MARCH 1
 #endif
@@ -669,15 +673,15 @@ unsigned grid_for(const hrt_handle* h, int64_t n) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)h->sm_count * 16));
 }
 
-template <int E, int F>
+template <int E, int F, int T = 1>
 int launch_ws(hrt_handle* h, const fws::SampleIn* in, fws::RowMap rm, int64_t n, const float4* dir32,
               float4* out, int density_only, const int32_t* round_ctr, cudaStream_t st) {
     constexpr uint32_t smem = fws::plan(E).total;
-    CK(cudaFuncSetAttribute(fws::k_field_ws<E, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(fws::k_field_ws<E, F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t tiles = (n + fws::kRows - 1) / fws::kRows;
     const int grid = round_ctr ? h->sm_count
                                : (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)h->sm_count));
-    fws::k_field_ws<E, F><<<grid, fws::kThreads, smem, st>>>(h->sc.field.nf, in, rm, n, dir32, out,
+    fws::k_field_ws<E, F, T><<<grid, fws::kThreads, smem, st>>>(h->sc.field.nf, in, rm, n, dir32, out,
                                                              density_only, round_ctr, h->ps.stats,
                                                              round_ctr ? h->round_rows : nullptr);
     CK(cudaGetLastError());
@@ -688,14 +692,21 @@ int launch_ws(hrt_handle* h, const fws::SampleIn* in, fws::RowMap rm, int64_t n,
 // field engine; bracketed by events so the dominant kernel's device time is
 // measured live.
 int field_ws(hrt_handle* h, const fws::SampleIn* in, fws::RowMap rm, int64_t n, const float4* dir32,
-             float4* out, int density_only, cudaStream_t st, const int32_t* round_ctr = nullptr) {
+             float4* out, int density_only, cudaStream_t st, const int32_t* round_ctr = nullptr,
+             bool teams = false) {
     if (n <= 0 && !round_ctr) return HRT_OK;
     const bool timed = h->n_timed < kTimedLaunches;
     if (timed) CK(cudaEventRecord(h->mev[2 * h->n_timed], st));
     int rc;
     switch (h->E * 8 + h->F) {
-        case 16 * 8 + 2: rc = launch_ws<16, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
-        case 32 * 8 + 2: rc = launch_ws<32, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
+        case 16 * 8 + 2:
+            rc = teams ? launch_ws<16, 2, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st)
+                       : launch_ws<16, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st);
+            break;
+        case 32 * 8 + 2:
+            rc = teams ? launch_ws<32, 2, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st)
+                       : launch_ws<32, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st);
+            break;
         case 64 * 8 + 4: rc = launch_ws<64, 4>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
         case 32 * 8 + 4: rc = launch_ws<32, 4>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
         case 64 * 8 + 2: rc = launch_ws<64, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
@@ -995,8 +1006,9 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
         const int32_t target = (int32_t)std::min<int64_t>((int64_t)h->sm_count * 128 * kTailTiles, 1 << 30);
         const int32_t cap = (int32_t)std::min<int64_t>(h->batch_cap, 1 << 30);
         const unsigned gsh = (unsigned)(h->sm_count * 16);
+        int32_t round = 0;                       // march round of this chunk
         while (true) {
-            for (int k = 0; k < kRoundsPerCheck; ++k) {
+            for (int k = 0; k < kRoundsPerCheck; ++k, ++round) {
                 pbeg(h, st, HRT_STAGE_COMPOSITE);
                 kern::k_round_begin<<<1, 1, 0, st>>>(h->ps.counters, h->ps.stats, target, cap,
                                                     h->round_rows, kTimedLaunches);
@@ -1005,8 +1017,9 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
                 CK(cudaGetLastError());
                 pend(h, HRT_STAGE_COMPOSITE, st);
                 pbeg(h, st, HRT_STAGE_FIELD);
+                // the first rounds carry the L1-coherent primary rays: two encode teams
                 if ((rc = field_ws(h, h->ms.in, fws::RowMap{}, 0, h->ms.dir32, h->ms.out, 0, st,
-                                   h->ps.counters)))
+                                   h->ps.counters, round < kTeamRounds)))
                     return rc;
                 pend(h, HRT_STAGE_FIELD, st);
                 if (h->sc.em.n > 0) {
