@@ -4,6 +4,7 @@ SASS page is mapped through nvdisasm's line table of the same library).
 
   ncu -i rep.ncu-rep --page source --csv --print-source sass > sass.csv
   python tools/sass_lines.py sass.csv path/to/libhrt.so <mangled kernel name> [top]
+(per line: share of stall samples, instructions executed, top two stall reasons)
 """
 import csv
 import os
@@ -20,10 +21,12 @@ rows = list(csv.reader(open(sass_csv)))
 h = rows[1]
 ai, ci = h.index("Address"), h.index("Warp Stall Sampling (All Samples)")
 ei = h.index("Instructions Executed")
+si = [k for k, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
 samples = []
 for r in rows[2:]:
     if len(r) > ci and r[ai].startswith("0x"):
-        samples.append((int(r[ai], 16), float(r[ci] or 0), float(r[ei] or 0)))
+        samples.append((int(r[ai], 16), float(r[ci] or 0), float(r[ei] or 0),
+                        [float(r[k] or 0) for k in si]))
 base = samples[0][0]
 
 tmp = tempfile.mkdtemp()
@@ -43,10 +46,16 @@ for ln in sec.splitlines():
     if m and cur:
         line_of[int(m.group(1), 16)] = cur
 agg, inst = defaultdict(float), defaultdict(float)
-for addr, s, e in samples:
+why = defaultdict(lambda: [0.0] * len(si))
+for addr, s, e, st in samples:
     k = line_of.get(addr - base, "?")
     agg[k] += s
     inst[k] += e
+    why[k] = [a + b for a, b in zip(why[k], st)]
 tot = sum(agg.values()) or 1
 for k, v in sorted(agg.items(), key=lambda x: -x[1])[:top]:
-    print(f"{100 * v / tot:5.1f}%  {k:28s} inst {inst[k]:.3g}")
+    w = why[k]
+    tw = sum(w) or 1
+    top2 = sorted(range(len(si)), key=lambda x: -w[x])[:2]
+    reasons = " ".join(f"{h[si[x]][6:]} {100 * w[x] / tw:.0f}%" for x in top2)
+    print(f"{100 * v / tot:5.1f}%  {k:28s} inst {inst[k]:.3g}  [{reasons}]")
