@@ -234,6 +234,8 @@ enum Counter { C_Q0 = 0, C_Q1 = 1, C_FETCH = 2,
                C_TAIL = 19,
                // march-round ordinal of this render call (k_round_begin; hrt_round_rows)
                C_RIDX = 20,
+               // k_paths_bounce: lengths of its two ping-pong path queues
+               C_PB0 = 21, C_PB1 = 22,
                C_COUNT = 16 };
 
 HRT_DEV d3 field_point(const DevField& f, d3 p) {

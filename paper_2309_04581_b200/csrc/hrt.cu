@@ -63,6 +63,10 @@ constexpr int kTexLevels = HRT_TEX_LEVELS;        // finest levels gathered via 
 #define HRT_TEAM_ROUNDS 3
 #endif
 constexpr int kTeamRounds = HRT_TEAM_ROUNDS;       // march rounds run with two encode teams (fws T = 2)
+#ifndef HRT_PATHS_BY_BOUNCE
+#define HRT_PATHS_BY_BOUNCE 1
+#endif
+constexpr bool kPathsByBounce = HRT_PATHS_BY_BOUNCE;   // k_paths_bounce per bounce (compacted) vs k_paths
 #ifndef HRT_MIXED_MARCH
 #define HRT_MIXED_MARCH 1
 #endif
@@ -1120,10 +1124,26 @@ int run_bounces(hrt_handle* h, kern::Args& a, int64_t paths, int mode, cudaStrea
         if ((rc = ensure_geo(h, h->sc.n_bounces))) return rc;
         pbeg(h, st, HRT_STAGE_INTERSECT);
         kern::k_reset_queue<<<1, 1, 0, st>>>(h->ps.counters, 1);
-        if (paths < kCoopPaths) kern::k_paths_coop<<<grid_for(h, paths * 4), kThreads, 0, st>>>(a, h->ms.geo);
-        else kern::k_paths<<<(unsigned)std::min<int64_t>((paths + HRT_PATHS_THREADS - 1) / HRT_PATHS_THREADS,
-                                                         (int64_t)h->sm_count * 16 * 256 / HRT_PATHS_THREADS),
-                             HRT_PATHS_THREADS, 0, st>>>(a, h->ms.geo);
+        const unsigned gp = (unsigned)std::min<int64_t>((paths + HRT_PATHS_THREADS - 1) / HRT_PATHS_THREADS,
+                                                        (int64_t)h->sm_count * 16 * 256 / HRT_PATHS_THREADS);
+        if (paths < kCoopPaths) {
+            kern::k_paths_coop<<<grid_for(h, paths * 4), kThreads, 0, st>>>(a, h->ms.geo);
+        } else if (kPathsByBounce) {
+            // bounce-b rays of the paths still going, compacted between launches
+            const int32_t* qin = h->ps.queue[0];
+            const int32_t* nin = h->ps.counters + C_Q0;
+            for (int b = 1; b <= h->sc.n_bounces; ++b) {
+                int32_t* qout = h->ms.mq[b & 1];
+                int32_t* nout = h->ps.counters + (b & 1 ? C_PB1 : C_PB0);
+                kern::k_reset_queue<<<1, 1, 0, st>>>(h->ps.counters, b & 1 ? C_PB1 : C_PB0);
+                kern::k_paths_bounce<<<gp, HRT_PATHS_THREADS, 0, st>>>(a, h->ms.geo, b, qin, nin, qout, nout);
+                h->launches += 2;
+                qin = qout;
+                nin = nout;
+            }
+        } else {
+            kern::k_paths<<<gp, HRT_PATHS_THREADS, 0, st>>>(a, h->ms.geo);
+        }
         CK(cudaGetLastError());
         pend(h, HRT_STAGE_INTERSECT, st);
         h->launches += 2;

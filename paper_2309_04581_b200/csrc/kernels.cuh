@@ -452,6 +452,40 @@ __global__ void __launch_bounds__(HRT_PATHS_THREADS, HRT_PATHS_MINB * 256 / HRT_
     if (blockIdx.x == 0 && threadIdx.x == 0) stat_add(s.stats, S_SEGMENTS, n);   // bounce-1 rays
 }
 
+// k_paths bounce by bounce: one launch per bounce b traces the bounce-b rays
+// of the paths in qin (bounce 1: every path of queue 0; later: the paths
+// whose bounce b-1 ray hit) and compacts the paths that go on into qout, so
+// a warp's lanes all carry live rays instead of idling once their own path
+// has missed. Same rays, hits and spawn arithmetic as k_paths.
+__global__ void __launch_bounds__(HRT_PATHS_THREADS, HRT_PATHS_MINB * 256 / HRT_PATHS_THREADS)
+k_paths_bounce(Args a, PathGeo g, int32_t b, const int32_t* __restrict__ qin, const int32_t* nin,
+               int32_t* __restrict__ qout, int32_t* nout) {
+    const int32_t n = *nin;
+    const PathState& s = a.ps;
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const int32_t p = qin[j];
+        const int64_t at = (int64_t)(b - 1) * g.cap + p;
+        const d3 o = b == 1 ? mk(s.ox[p], s.oy[p], s.oz[p]) : mk(g.ox[at], g.oy[at], g.oz[at]);
+        const d3 d = b == 1 ? mk(s.dx[p], s.dy[p], s.dz[p]) : mk(g.dx[at], g.dy[at], g.dz[at]);
+        double t = INFINITY;
+        const int32_t f = bvh::nearest(a.sc.bvh, o, d, 0.0, INFINITY, t);
+        g.t[at] = t;
+        g.face[at] = f;
+        if (b == 1) {
+            s.t_hit[p] = t;
+            s.face[p] = f;
+        }
+        if (f < 0 || b == a.sc.n_bounces) continue;
+        d3 o2, d2;
+        spawn_ray(a, s.pix[p], s.smp[p], b, o, d, t, f, o2, d2);
+        const int64_t nx = at + g.cap;
+        g.ox[nx] = o2.x; g.oy[nx] = o2.y; g.oz[nx] = o2.z;
+        g.dx[nx] = d2.x; g.dy[nx] = d2.y; g.dz[nx] = d2.z;
+        qout[reserve(nout)] = p;
+    }
+    if (b == 1 && blockIdx.x == 0 && threadIdx.x == 0) stat_add(s.stats, S_SEGMENTS, n);   // bounce-1 rays
+}
+
 // k_paths with 4 lanes per path (bvh::closest_q_coop), for chunks of few
 // paths where the longest per-path chain of traversals bounds the launch.
 __global__ void __launch_bounds__(256) k_paths_coop(Args a, PathGeo g) {
