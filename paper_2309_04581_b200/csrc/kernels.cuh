@@ -1006,18 +1006,33 @@ __global__ void __launch_bounds__(HRT_STEP_THREADS, HRT_STEP_MINB * 256 / HRT_ST
 #ifndef HRT_SHADOW_MINB
 #define HRT_SHADOW_MINB 4
 #endif
+#ifndef HRT_SHADOW_PATH_MAJOR
+#define HRT_SHADOW_PATH_MAJOR 1
+#endif
+constexpr bool kShadowPathMajor = HRT_SHADOW_PATH_MAJOR;
 __global__ void __launch_bounds__(256, HRT_SHADOW_MINB) k_shadow(Args a, MarchState m, fws::RowMap rm, int64_t rows,
                                                              int32_t dev_rows) {
     const PathState& s = a.ps;
+    uint32_t S = 0;
     if (dev_rows) {                  // device-driven round: this round's batch shape
         const int32_t* ctr = a.ps.counters;
         fws::set_rows(rm, ctr[C_MQ0 + (ctr[C_CUR] ^ 1)], ctr[C_STRIDE]);
-        rows = (int64_t)rm.width * ctr[C_S];
+        S = (uint32_t)ctr[C_S];
+        rows = (int64_t)rm.width * S;
     }
     int32_t cast = 0;
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < rows;
          l += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = fws::phys_row(rm, l);
+        int64_t li = l;
+        if (kShadowPathMajor && S > 0) {
+            // path-major walk (a warp takes consecutive samples of one or two
+            // paths): the path state loads are shared, and the queue gets the
+            // rays of a path's consecutive samples side by side - similar
+            // origins in one tracer warp, which keeps its node fetches in L1
+            const uint32_t jj = (uint32_t)l / S;
+            li = (int64_t)((uint32_t)l - jj * S) * rm.width + jj;
+        }
+        const int64_t row = fws::phys_row(rm, li);
         const int32_t p = m.in[row].path;
         if (p < 0) continue;
         const float4 f = m.out[row];

@@ -118,6 +118,35 @@ def test_gpu_neural_shadows_hdr(cuda):
     r.close()
 
 
+def test_shadowed_frame_pipelines_agree_at_scale(cuda):
+    """A wide shadowed frame (the shadow scene at 256 x 192 x 8 spp: 393k
+    paths, batches of millions of rows, thousands of warps per round): the
+    device-driven march - shadow rays set up when the samples are generated,
+    their codes double-buffered against the previous batch's composite -
+    equals the unfused trace-mode pipeline (generate -> field -> shadow
+    set-up -> trace -> composite, one kernel each) bit for bit, in the
+    continuous and in the bounce-by-bounce march, with equal sample and
+    shadow-ray counts."""
+    scene = shadow_scene()
+    scene.camera = Camera(configs.look_at_safe((0.0, 0.3, 4.0)), math.radians(40.0), (256, 192))
+    imgs, stats = [], []
+    for mode in ("continuous", "bounce", "unfused"):
+        r = Renderer(scene)
+        if mode == "bounce":
+            r.set_march(False)
+        if mode == "unfused":
+            rec = torch.zeros((16, 4), dtype=torch.int32, device=cuda)
+            r.set_trace(rec, 16)
+        imgs.append(r.render_pixels(scene.camera, 8, 3).cpu().numpy())
+        stats.append(dict(r.last_stats))
+        r.close()
+    assert stats[0]["shadow_rays"] > 1_000_000
+    for img, st in zip(imgs[1:], stats[1:]):
+        assert np.array_equal(imgs[0], img)
+        assert st["nerf_samples"] == stats[0]["nerf_samples"]
+        assert st["shadow_rays"] == stats[0]["shadow_rays"]
+
+
 def test_gpu_cfg2_lambertian_crop(cuda):
     """cfg2: diffuse plane + 50k-triangle blob lit only by the NeRF, 16 spp
     stratified. The GPU reuses the reference RNG streams, so paths match the
