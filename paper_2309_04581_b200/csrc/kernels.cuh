@@ -943,8 +943,10 @@ HRT_DEV void step_tail(const Args& a, const MarchState& m, int32_t first, int32_
     }
 }
 
+// 64 registers (8 blocks of 128 per SM, ~200 B of spills) beats 80 (6 blocks, 84 B):
+// cfg3 composite 23.1 -> 21.4 ms; cfg1 and cfg4 equal
 #ifndef HRT_STEP_MINB
-#define HRT_STEP_MINB 3
+#define HRT_STEP_MINB 4
 #endif
 template <bool kMixed>
 #ifndef HRT_STEP_THREADS
