@@ -656,7 +656,7 @@ def run_ours(args, rank, world, local):
                                          for i in np.nonzero(live)[0][:8]],
         "note": "hrt_round_rows of the profiled frame (first chunk's rounds): the first rounds carry the "
                 "coherent primary rays, the later ones the incoherent bounces (DESIGN 4.1)"}
-    gather_gbs = wl.r.gather_peak(2) if wl.field.n_features == 2 else None   # (8-B gather probe: F = 2)
+    gather_gbs = wl.r.gather_peak(2)          # random one-entry gathers (8 B F = 2, 16 B F = 4), LSU + TEX
     l2 = wl.r.l2_peak()
 
     extra = None
@@ -683,9 +683,11 @@ def run_ours(args, rank, world, local):
         traffic, traffic_src = ncu_traffic(args.config)
         traffic = traffic or {}
         req_per_sample = traffic.get("l2_requests_per_sample")
-        peak_requests = gather_gbs * 1e9 / 8.0 if gather_gbs else None    # one request per random 8-B gather
+        entry_bytes = 4 * field.n_features
+        peak_requests = gather_gbs * 1e9 / entry_bytes if gather_gbs else None   # one request per random gather
         table_bytes = int(field.table.nbytes)
         roof_peak = l2["read_gbs"]
+        gather_frac = field_sps * req_per_sample / peak_requests if req_per_sample and peak_requests else None
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
@@ -707,8 +709,8 @@ def run_ours(args, rank, world, local):
             "gpu_launches": int(rank0["launches"]),
             "roofline": {
                 "bound": "l2",
-                "kernel": f"fws::k_field_ws<{field.enc_dim},{field.n_features}> (warp-specialized hash encode + "
-                          "5-layer tcgen05 MLP, TMEM operands)",
+                "kernel": f"fws::k_field_ws<{field.enc_dim},{field.n_features},T> (warp-specialized hash encode + "
+                          "5-layer tcgen05 MLP, TMEM operands; T = 2 encode teams in the first march rounds)",
                 "achieved": achieved, "peak": roof_peak, "unit": "GB/s",
                 "frac": achieved / roof_peak,
                 "traffic": traffic.get("dram_bytes_per_launch"),
@@ -728,11 +730,11 @@ def run_ours(args, rank, world, local):
                 "bound": "L1 miss requests to L2 (random gathers, ~1 request/clk/SM)",
                 "achieved": field_sps * req_per_sample if req_per_sample else None,
                 "peak": peak_requests, "unit": "requests/s",
-                "frac": field_sps * req_per_sample / peak_requests if req_per_sample and peak_requests else None,
+                "frac": gather_frac,
                 "requests_per_sample": req_per_sample,
                 "sectors_per_sample": traffic.get("l2_sectors_per_sample"),
                 "random_sector_gbs": l2["gather_sector_gbs"],
-                "peak_source": "hrt_gather_peak (live, this run): independent random 8-B gathers over the "
+                "peak_source": f"hrt_gather_peak (live, this run): independent random {entry_bytes}-B gathers over the "
                                f"same table, {gather_gbs or 0:.0f} GB/s useful = 1 request each; requests/sample from "
                                f"{traffic_src} (ncu lts__t_requests_srcunit_tex_op_read over every field-engine "
                                f"launch of one frame, commit {traffic.get('commit')})",
@@ -752,6 +754,25 @@ def run_ours(args, rank, world, local):
                           "note": "one untimed frame with hrt_set_profile (event pair per launch)"},
             "field_rounds": rounds_block,
         }
+        if achieved > roof_peak and gather_frac is not None:
+            # The 344 MiB cfg4 table does not fit L2 and L1 serves most of the algorithmic
+            # gather bytes, so bytes / L2 peak exceeds 1 and is no efficiency: the binding
+            # roof is then the random-gather request path, in the same GB/s units (useful
+            # table bytes per request, as the live probe counts them).
+            alg = line["roofline"]
+            line["roofline"] = {
+                "bound": "l2", "kernel": alg["kernel"],
+                "achieved": field_sps * req_per_sample * entry_bytes / 1e9, "peak": gather_gbs, "unit": "GB/s",
+                "frac": gather_frac, "traffic": alg["traffic"], "launches": alg["launches"],
+                "avg_launch_ms": alg["avg_launch_ms"],
+                "peak_source": f"hrt_gather_peak (live, this run): random {entry_bytes}-B gathers over the table, "
+                               f"LSU + TEX; achieved = L2 requests/sample ({req_per_sample:.2f}, ncu, "
+                               f"{traffic_src}, commit {traffic.get('commit')}) x {entry_bytes} B x field-engine "
+                               "samples/s; the algorithmic-bytes view exceeds the L2 peak (L1 hits) and is kept "
+                               "under 'algorithmic'",
+                "algorithmic": {"achieved": achieved, "peak": roof_peak, "frac": achieved / roof_peak,
+                                "bytes_per_sample": enc_bytes},
+                "hbm": alg["hbm"]}
         if extra:
             line["cfg1"] = extra
         if world == 1 and not args.no_cpu_baseline:

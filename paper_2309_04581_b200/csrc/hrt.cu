@@ -63,6 +63,10 @@ constexpr int kTexLevels = HRT_TEX_LEVELS;        // finest levels gathered via 
 #define HRT_TEAM_ROUNDS 3
 #endif
 constexpr int kTeamRounds = HRT_TEAM_ROUNDS;       // march rounds run with two encode teams (fws T = 2)
+#ifndef HRT_TEAMS_F4
+#define HRT_TEAMS_F4 0
+#endif
+constexpr bool kTeamsF4 = HRT_TEAMS_F4;            // encode teams also for F = 4 fields (cfg4)
 #ifndef HRT_PATHS_BY_BOUNCE
 #define HRT_PATHS_BY_BOUNCE 1
 #endif
@@ -711,7 +715,10 @@ int field_ws(hrt_handle* h, const fws::SampleIn* in, fws::RowMap rm, int64_t n, 
             rc = teams ? launch_ws<32, 2, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st)
                        : launch_ws<32, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st);
             break;
-        case 64 * 8 + 4: rc = launch_ws<64, 4>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
+        case 64 * 8 + 4:
+            rc = teams && kTeamsF4 ? launch_ws<64, 4, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st)
+                                   : launch_ws<64, 4>(h, in, rm, n, dir32, out, density_only, round_ctr, st);
+            break;
         case 32 * 8 + 4: rc = launch_ws<32, 4>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
         case 64 * 8 + 2: rc = launch_ws<64, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
         case 16 * 8 + 4: rc = launch_ws<16, 4>(h, in, rm, n, dir32, out, density_only, round_ctr, st); break;
@@ -1782,19 +1789,24 @@ int hrt_ipc_close(void* ptr) {
 
 int hrt_gather_peak(hrt_handle* h, int32_t mode, double* gbs) {
     if (!h || !gbs) return fail(HRT_EINVAL, "null argument");
-    if (h->sc.field.kind != HRT_FIELD_NEURAL || h->F != 2) return fail(HRT_EINVAL, "needs an F=2 neural field");
+    if (h->sc.field.kind != HRT_FIELD_NEURAL || (h->F != 2 && h->F != 4))
+        return fail(HRT_EINVAL, "needs a neural field (F = 2 or 4)");
     if (mode < 0 || mode > 2) return fail(HRT_EINVAL, "mode: 0 LSU, 1 TEX, 2 both");
     const NeuralField& nf = h->sc.field.nf;
     const uint32_t n = (uint32_t)h->tab_entries;
     float* sink = nullptr;
     CK(cudaMalloc(&sink, 4));
     const int threads = 512, blocks = h->sm_count * 4, iters = 64;
-    const float2* tab = reinterpret_cast<const float2*>(nf.table);
+    const float2* tab2 = reinterpret_cast<const float2*>(nf.table);
+    const float4* tab4 = reinterpret_cast<const float4*>(nf.table);
+    const bool f4 = h->F == 4;
     cudaStream_t s2 = nullptr;
     CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
     auto launch = [&](cudaStream_t st, bool tex) {
-        if (tex) probe::k_gather<true><<<blocks, threads, 0, st>>>(tab, nf.tex, n, iters, sink);
-        else probe::k_gather<false><<<blocks, threads, 0, st>>>(tab, nf.tex, n, iters, sink);
+        if (f4 && tex) probe::k_gather<true><<<blocks, threads, 0, st>>>(tab4, nf.tex, n, iters, sink);
+        else if (f4) probe::k_gather<false><<<blocks, threads, 0, st>>>(tab4, nf.tex, n, iters, sink);
+        else if (tex) probe::k_gather<true><<<blocks, threads, 0, st>>>(tab2, nf.tex, n, iters, sink);
+        else probe::k_gather<false><<<blocks, threads, 0, st>>>(tab2, nf.tex, n, iters, sink);
     };
     auto run = [&]() {       // mode 2: LSU and TEX kernels side by side on two streams
         if (mode == 2) {
@@ -1824,7 +1836,7 @@ int hrt_gather_peak(hrt_handle* h, int32_t mode, double* gbs) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     const double loads = (double)blocks * threads * iters * 8 * reps * (mode == 2 ? 2 : 1);
-    *gbs = loads * 8.0 / (ms * 1e-3) / 1e9;            // useful bytes: 8 B per gather
+    *gbs = loads * (f4 ? 16.0 : 8.0) / (ms * 1e-3) / 1e9;   // useful bytes: one entry per gather
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaStreamDestroy(s2);

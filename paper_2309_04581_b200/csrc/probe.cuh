@@ -2,7 +2,8 @@
 // hash-grid encode. The encode is bound by random 8-byte gathers from the
 // L2-resident table (ncu: L1 miss-request path ~87 % busy), so its peak is
 // measured here on the same table: every thread issues independent gathers
-// at pseudo-random entries (LSU or TEX path), 8 in flight.
+// at pseudo-random entries (LSU or TEX path), 8 in flight, one table entry
+// (8 B for F = 2, 16 B for F = 4) each.
 #pragma once
 #include "common.cuh"
 
@@ -12,18 +13,19 @@ HRT_DEV uint32_t mix32(uint32_t x) {
     x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; return x ^ (x >> 16);
 }
 
-template <bool kTex>
-__global__ void __launch_bounds__(512) k_gather(const float2* __restrict__ table,
+// V = float2 (F = 2, 8-B entries) or float4 (F = 4, 16-B entries).
+template <bool kTex, typename V>
+__global__ void __launch_bounds__(512) k_gather(const V* __restrict__ table,
                                                  unsigned long long tex, uint32_t n_entries,
                                                  int32_t iters, float* sink) {
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
     float acc = 0.f;
     for (int32_t it = 0; it < iters; ++it) {
-        float2 v[8];
+        V v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const uint32_t idx = mix32(tid * 0x9E3779B9U + (uint32_t)(it * 8 + u)) % n_entries;
-            v[u] = kTex ? tex1Dfetch<float2>(tex, (int)idx) : __ldg(table + idx);
+            v[u] = kTex ? tex1Dfetch<V>(tex, (int)idx) : __ldg(table + idx);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y;

@@ -228,8 +228,9 @@ class Renderer:
         _lib.check(self.lib.hrt_set_profile(self.handle, int(bool(on))), "hrt_set_profile")
 
     def gather_peak(self, mode=2):
-        """Measured random 8-byte gather rate (useful GB/s) over this scene's
-        hash table: the roofline of the encode (hrt_gather_peak)."""
+        """Measured random one-entry gather rate (useful GB/s; 8-B entries for
+        F = 2, 16-B for F = 4) over this scene's hash table: the roofline of
+        the encode (hrt_gather_peak)."""
         v = ctypes.c_double(0.0)
         _lib.check(self.lib.hrt_gather_peak(self.handle, int(mode), ctypes.byref(v)), "hrt_gather_peak")
         return v.value

@@ -9,7 +9,7 @@ l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum,l1tex__t_sector_hit_rate.pct \
       python tools/quick_bench.py 3 1920x1080 8 1
 
   python tools/field_traffic.py field.csv <evaluated samples of that frame> \
-      profiles/rNN_field_traffic_cfg3.json cfg3 <commit>
+      profiles/rNN_field_traffic_cfg3.json cfg3 <commit> [kernel label]
 
 The first k_field_ws launch of a renderer is the occupancy-grid build
 (density only), not a march round: it is listed but excluded from the
@@ -46,7 +46,7 @@ def req_per_clk(d):
 
 
 out = {
-    "kernel": "fws::k_field_ws<32,2>",
+    "kernel": sys.argv[6] if len(sys.argv) > 6 else "fws::k_field_ws<32,2,T> (T = 2: encode teams, first 3 march rounds of a chunk)",
     "config": config,
     "commit": commit,
     "capture": "ncu --metrics gpu__time_duration.sum,lts__t_sectors_srcunit_tex_op_read.sum,"
