@@ -63,10 +63,17 @@ constexpr int kTexLevels = HRT_TEX_LEVELS;        // finest levels gathered via 
 #define HRT_TEAM_ROUNDS 3
 #endif
 constexpr int kTeamRounds = HRT_TEAM_ROUNDS;       // march rounds run with two encode teams (fws T = 2)
-#ifndef HRT_TEAMS_F4
-#define HRT_TEAMS_F4 0
+#ifndef HRT_TEAM_ROUNDS_F4
+#define HRT_TEAM_ROUNDS_F4 5
 #endif
-constexpr bool kTeamsF4 = HRT_TEAMS_F4;            // encode teams also for F = 4 fields (cfg4)
+constexpr int kTeamRoundsF4 = HRT_TEAM_ROUNDS_F4;  // ... for F = 4 fields (cfg4 960x540x64: 3 / 5 / 8 rounds
+                                                   // 640 / 631 / 640 ms field)
+// encode teams also for F = 4 fields (cfg4 960x540x64: field 670 -> 641 ms, despite
+// 76 B of spills in k_field_ws<64, 4, 2>)
+#ifndef HRT_TEAMS_F4
+#define HRT_TEAMS_F4 1
+#endif
+constexpr bool kTeamsF4 = HRT_TEAMS_F4;
 #ifndef HRT_PATHS_BY_BOUNCE
 #define HRT_PATHS_BY_BOUNCE 1
 #endif
@@ -1030,7 +1037,7 @@ int march_neural(hrt_handle* h, const kern::Args& a, int64_t n_paths, cudaStream
                 pbeg(h, st, HRT_STAGE_FIELD);
                 // the first rounds carry the L1-coherent primary rays: two encode teams
                 if ((rc = field_ws(h, h->ms.in, fws::RowMap{}, 0, h->ms.dir32, h->ms.out, 0, st,
-                                   h->ps.counters, round < kTeamRounds)))
+                                   h->ps.counters, round < (h->F == 4 ? kTeamRoundsF4 : kTeamRounds))))
                     return rc;
                 pend(h, HRT_STAGE_FIELD, st);
                 if (h->sc.em.n > 0) {
