@@ -718,4 +718,109 @@ __global__ void k_qsync(QNode* q, const int4* __restrict__ src, const BvhNode* _
     }
 }
 
+
+// ------------------------------------------------- shadow entry table
+// Light-space culling of shadow any-hit queries, exact. A shadow ray from a
+// point x in world cell C towards a light point q in patch Q of emitter e
+// (q is bilinear in (sqrt(u1), u2), so a patch's points lie in the convex
+// hull of its 4 corner points) stays inside H = hull(C u Q); a triangle it
+// hits meets H, and so does every tree box above that triangle. The entry of
+// (C, e, Q) is found from the root by descending while exactly one child box
+// can meet H; it is -2 when no child box can meet H (nothing can be hit).
+// Separation is shown on 7 axes (x, y, z and four across the beam C -> Q) in
+// float64 with H padded: an axis only ever proves a real separation, so a
+// traversal started at the entry finds every hit a traversal from the root
+// finds (and the blocked / visible answer is identical).
+struct Hull {
+    d3 ax[7];
+    double lo[7], hi[7];
+};
+
+HRT_DEV bool hull_apart(const Hull& H, float lx, float ly, float lz, float hx, float hy, float hz) {
+    const double cx = 0.5 * ((double)lx + (double)hx), cy = 0.5 * ((double)ly + (double)hy),
+                 cz = 0.5 * ((double)lz + (double)hz);
+    const double ex = 0.5 * ((double)hx - (double)lx), ey = 0.5 * ((double)hy - (double)ly),
+                 ez = 0.5 * ((double)hz - (double)lz);
+#pragma unroll
+    for (int a = 0; a < 7; ++a) {
+        const d3 n = H.ax[a];
+        const double c = n.x * cx + n.y * cy + n.z * cz;
+        const double r = fabs(n.x) * ex + fabs(n.y) * ey + fabs(n.z) * ez;
+        if (c + r < H.lo[a] || c - r > H.hi[a]) return true;
+    }
+    return false;
+}
+
+// entry index -> ((cell * n_emitters + emitter) * P + v) * P + u, cell = (z * g + y) * g + x
+__global__ void k_shadow_entry(DevBvh b, DevEmitters em, d3 glo, d3 cell, int32_t g, int32_t P,
+                               int32_t* out, int64_t n) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t pu = (int32_t)(e % P), pv = (int32_t)((e / P) % P);
+        const int64_t rest = e / ((int64_t)P * P);
+        const int32_t emi = (int32_t)(rest % em.n);
+        const int64_t c = rest / em.n;
+        const int32_t ci[3] = {(int32_t)(c % g), (int32_t)((c / g) % g), (int32_t)(c / ((int64_t)g * g))};
+        d3 V[12];
+        for (int k = 0; k < 8; ++k)
+            V[k] = mk(glo.x + (ci[0] + (k & 1)) * cell.x, glo.y + (ci[1] + ((k >> 1) & 1)) * cell.y,
+                      glo.z + (ci[2] + (k >> 2)) * cell.z);
+        const double* t = em.tris + 9 * emi;
+        for (int k = 0; k < 4; ++k) {
+            const double su = (double)(pu + (k & 1)) / P, u2 = (double)(pv + (k >> 1)) / P;
+            const double b0 = 1.0 - su, b1 = su * (1.0 - u2), b2 = su * u2;
+            V[8 + k] = mk(b0 * t[0] + b1 * t[3] + b2 * t[6], b0 * t[1] + b1 * t[4] + b2 * t[7],
+                          b0 * t[2] + b1 * t[5] + b2 * t[8]);
+        }
+        d3 cc = mk(0, 0, 0), pc = mk(0, 0, 0);
+        double big = 1.0;
+        for (int k = 0; k < 12; ++k) {
+            if (k < 8) cc = add(cc, scale(V[k], 0.125)); else pc = add(pc, scale(V[k], 0.25));
+            big = fmax(big, fmax(fabs(V[k].x), fmax(fabs(V[k].y), fabs(V[k].z))));
+        }
+        const double pad = 1e-6 * big;
+        Hull H;
+        H.ax[0] = mk(1, 0, 0); H.ax[1] = mk(0, 1, 0); H.ax[2] = mk(0, 0, 1);
+        d3 D = sub(pc, cc);
+        const double dl = norm(D);
+        D = dl > 1e-12 ? scale(D, 1.0 / dl) : mk(1, 0, 0);
+        const d3 ek = (fabs(D.x) <= fabs(D.y) && fabs(D.x) <= fabs(D.z)) ? mk(1, 0, 0)
+                      : (fabs(D.y) <= fabs(D.z) ? mk(0, 1, 0) : mk(0, 0, 1));
+        d3 U = cross(D, ek);
+        U = scale(U, 1.0 / norm(U));
+        const d3 W = cross(D, U);
+        H.ax[3] = U; H.ax[4] = W;
+        H.ax[5] = scale(add(U, W), 0.7071067811865476);
+        H.ax[6] = scale(sub(U, W), 0.7071067811865476);
+        for (int a = 0; a < 7; ++a) {
+            double lo = INFINITY, hi = -INFINITY;
+            for (int k = 0; k < 12; ++k) {
+                const double v = dot(H.ax[a], V[k]);
+                lo = fmin(lo, v);
+                hi = fmax(hi, v);
+            }
+            const double w = pad * (fabs(H.ax[a].x) + fabs(H.ax[a].y) + fabs(H.ax[a].z)) + 1e-12 * big;
+            H.lo[a] = lo - w;
+            H.hi[a] = hi + w;
+        }
+        int32_t node = 0, res = -2;
+        if (b.n_faces > 0) {
+            while (true) {
+                const QNode q = load_q(b, node);
+                const float lx[4] = {q.lox.x, q.lox.y, q.lox.z, q.lox.w}, ly[4] = {q.loy.x, q.loy.y, q.loy.z, q.loy.w};
+                const float lz[4] = {q.loz.x, q.loz.y, q.loz.z, q.loz.w}, hx[4] = {q.hix.x, q.hix.y, q.hix.z, q.hix.w};
+                const float hy[4] = {q.hiy.x, q.hiy.y, q.hiy.z, q.hiy.w}, hz[4] = {q.hiz.x, q.hiz.y, q.hiz.z, q.hiz.w};
+                int cnt = 0, only = -1;
+                for (int k = 0; k < 4; ++k)
+                    if (!hull_apart(H, lx[k], ly[k], lz[k], hx[k], hy[k], hz[k])) { ++cnt; only = k; }
+                if (cnt == 0) { res = -2; break; }
+                if (cnt == 1 && qref(q, only) >= 0) { node = qref(q, only); continue; }
+                res = node;
+                break;
+            }
+        }
+        out[e] = res;
+    }
+}
+
 }  // namespace bvh

@@ -193,6 +193,14 @@ struct DevScene {
     int32_t n_bounces;
     double threshold, march_step, spawn_eps, early_t;
     int32_t sample_cap;
+    // Shadow entry table (bvh::k_shadow_entry, hrt.cu ensure_shadow_entry):
+    // for every cell of a g^3 world grid over the field box x emitter x
+    // light patch (p x p cells of the (sqrt(u1), u2) sample square), the
+    // blocker-tree node under which every triangle that a shadow ray from
+    // the cell to the patch can hit lies (-2: none can be hit). Null: off.
+    const int32_t* shent;
+    int32_t shent_g, shent_p;
+    double shent_lo[3], shent_inv[3];
 };
 
 // SoA per-path state for one wavefront chunk.

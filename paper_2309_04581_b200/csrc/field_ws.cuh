@@ -56,6 +56,12 @@ __device__ unsigned long long ws_prof[8];
 #define HRT_SYNTH_ENCODE 0
 #endif
 constexpr bool kSynthEncode = HRT_SYNTH_ENCODE;   // measurement build: MLP fed without gathers
+#ifndef HRT_SYNTH_MLP
+#define HRT_SYNTH_MLP 0
+#endif
+// measurement build: encoded tiles are released without MMAs and every row
+// gets (sigma, rgb) = (1, 0.5, 0.5, 0.5) - what the encode sustains alone
+constexpr bool kSynthMlp = HRT_SYNTH_MLP;
 constexpr int kEncWarps = 16;               // 4 level quarters x 4 lane quarters
 // Encode teams (template T): with T = 2 the 16 encode warps form two teams
 // of 8 (2 level halves x 4 lane quarters, one level of gathers in flight per
@@ -309,6 +315,14 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
         int it = 0;
         for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
             if ((it % kMlpGroups) != g) continue;
+            if constexpr (kSynthMlp) {
+                const int64_t l = t * kRows + m;
+                if (l < n) {
+                    const int64_t i = phys_row(rmap, l);
+                    if (in[i].path >= 0) __stcs(out + i, make_float4(1.f, .5f, .5f, .5f));
+                }
+                continue;
+            }
             const int64_t l = t * kRows + m;
             const int64_t i = l < n ? phys_row(rmap, l) : 0;
             float3 dir = make_float3(0.f, 0.f, 1.f);
@@ -361,7 +375,7 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
         // Walks tile pairs (one per group) layer by layer so one group's MMA
         // overlaps the other group's epilogue.
         const uint32_t wb = umma::saddr(smem + P.w);
-        const int nl = density_only ? 2 : 5;
+        const int nl = kSynthMlp ? 1 : (density_only ? 2 : 5);
         const uint32_t boff[5] = {W.d1, W.d2, W.c1, W.c2, W.c3};
         const int kdim[5] = {E, 64, 32, 64, 64};
         const int ndim[5] = {64, 16, 64, 64, 16};
@@ -382,6 +396,11 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
                         WS_T0(tf);
                         umma::mbar_wait(bar_full(bars, s), (uint32_t)((j / kStages) & 1));
                         WS_ADD(5, tf);
+                        if constexpr (kSynthMlp) {
+                            umma::fence_after();
+                            arrive(bar_empty(bars, s));
+                            continue;
+                        }
                         WS_T0(ta);
                         if (!fresh[g]) { umma::mbar_wait(actr, rph[g]); rph[g] ^= 1u; }
                         WS_ADD(6, ta);

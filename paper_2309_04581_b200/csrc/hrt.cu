@@ -161,6 +161,12 @@ struct hrt_handle {
     // hrt_set_profile: event pair per launch, folded into stage_ms
     bool prof = false;
     bool continuous = kMixedMarch;   // hrt_set_march
+    // shadow entry table (bvh::k_shadow_entry): rebuilt when the blocker
+    // tree or the field placement changed (geo_ver) since it was made
+    int32_t* shent = nullptr;
+    int64_t shent_n = 0;
+    int64_t geo_ver = 0, shent_ver = -1;
+    bool shent_on = true;            // HRT_SHADOW_ENTRY=0 at create: off
     void* geo_arena = nullptr;       // kern::PathGeo storage (ensure_geo)
     int64_t geo_n = 0;
     std::vector<cudaEvent_t> pev;
@@ -194,6 +200,7 @@ struct hrt_handle {
         for (cudaEvent_t e : pev) cudaEventDestroy(e);
         if (pinned) cudaFreeHost(pinned);
         if (rigid_xf) cudaFree(rigid_xf);
+        if (shent) cudaFree(shent);
         if (io_pix) cudaFree(io_pix);
         if (io_out) cudaFree(io_out);
         if (io_pix_host) cudaFreeHost(io_pix_host);
@@ -235,6 +242,7 @@ int refit_gpu(hrt_handle* h, const hrt::BvhHost& b, RefitState& r, DevBvh& dev, 
 
 // Refit from faces already in r.src (v0 | e1 | e2, global face order).
 int refit_from_src(hrt_handle* h, const hrt::BvhHost& b, RefitState& r, DevBvh& dev) {
+    ++h->geo_ver;
     const size_t n3 = 3 * (size_t)b.n_faces;
     CK(cudaMemset(r.visits, 0, b.nodes.size() * 4));
     const unsigned g1 = (unsigned)std::min<int64_t>((b.n_faces + 255) / 256, 148 * 16);
@@ -509,6 +517,7 @@ void build_wnodes(const hrt::BvhHost& b, std::vector<WNode>& w, std::vector<int2
 }
 
 int upload_bvh(hrt_handle* h, const hrt::BvhHost& b, DevBvh& out, RefitState& r) {
+    ++h->geo_ver;
     out.n_faces = b.n_faces;
     out.nodes = nullptr; out.tri = nullptr; out.tri_id = nullptr; out.wnodes = nullptr; out.qnodes = nullptr;
     out.qtex = 0;
@@ -1181,6 +1190,82 @@ int run_bounces(hrt_handle* h, kern::Args& a, int64_t paths, int mode, cudaStrea
     return HRT_OK;
 }
 
+// Shadow entry table (bvh::k_shadow_entry) over a 32^3 world grid around
+// the field box, per emitter and light patch; made when the scene has
+// emitters and blockers, remade after a blocker refit or a field move.
+#ifndef HRT_SHENT_G
+#define HRT_SHENT_G 32
+#endif
+#ifndef HRT_SHENT_P
+#define HRT_SHENT_P 8
+#endif
+constexpr int32_t kShentGrid = HRT_SHENT_G;
+int ensure_shadow_entry(hrt_handle* h) {
+    DevScene& sc = h->sc;
+    const bool want = h->shent_on && HRT_BVH_WIDTH == 4 && sc.em.n > 0 && sc.em.n <= 16 &&
+                      sc.blockers.n_faces > 0 && sc.field.kind != HRT_FIELD_NONE &&
+                      h->rfb.n_q < (1 << 23);
+    if (!want) {
+        sc.shent = nullptr;
+        return HRT_OK;
+    }
+    if (h->shent_ver == h->geo_ver && sc.shent) return HRT_OK;
+    const DevField& f = sc.field;
+    // world box of the field box (field_from_world is affine: invert its 3x3)
+    double lo[3] = {f.lo[0], f.lo[1], f.lo[2]}, hi[3] = {f.hi[0], f.hi[1], f.hi[2]};
+    if (!f.identity) {
+        const double* m = f.inv;
+        const double a = m[0], b = m[1], c = m[2], d = m[4], e = m[5], g = m[6], k = m[8], l = m[9], n = m[10];
+        const double det = a * (e * n - g * l) - b * (d * n - g * k) + c * (d * l - e * k);
+        if (!(std::fabs(det) > 1e-300)) { sc.shent = nullptr; return HRT_OK; }
+        const double R[9] = {(e * n - g * l) / det, (c * l - b * n) / det, (b * g - c * e) / det,
+                             (g * k - d * n) / det, (a * n - c * k) / det, (c * d - a * g) / det,
+                             (d * l - e * k) / det, (b * k - a * l) / det, (a * e - b * d) / det};
+        const double t[3] = {m[3], m[7], m[11]};
+        for (int ax = 0; ax < 3; ++ax) { lo[ax] = INFINITY; hi[ax] = -INFINITY; }
+        for (int q = 0; q < 8; ++q) {
+            const double pf[3] = {(q & 1) ? f.hi[0] : f.lo[0], (q & 2) ? f.hi[1] : f.lo[1],
+                                  (q & 4) ? f.hi[2] : f.lo[2]};
+            for (int ax = 0; ax < 3; ++ax) {
+                double w = 0.0;
+                for (int j = 0; j < 3; ++j) w += R[3 * ax + j] * (pf[j] - t[j]);
+                lo[ax] = std::min(lo[ax], w);
+                hi[ax] = std::max(hi[ax], w);
+            }
+        }
+    }
+    const int32_t g = kShentGrid, P = sc.em.n <= 4 ? HRT_SHENT_P : 4;
+    d3 glo, cell;
+    double inv[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        const double span = hi[ax] - lo[ax];
+        const double pad = 1e-3 * std::max(1.0, span);       // sample points on the box faces fall inside
+        const double l0 = lo[ax] - pad, c = (span + 2 * pad) / g;
+        (&glo.x)[ax] = l0;
+        (&cell.x)[ax] = c;
+        inv[ax] = 1.0 / c;
+        sc.shent_lo[ax] = l0;
+        sc.shent_inv[ax] = inv[ax];
+    }
+    const int64_t n = (int64_t)g * g * g * sc.em.n * P * P;
+    if (n > h->shent_n) {
+        if (h->shent) cudaFree(h->shent);
+        h->shent = nullptr;
+        h->shent_n = 0;
+        CK(cudaMalloc(&h->shent, (size_t)n * 4));
+        h->shent_n = n;
+    }
+    bvh::k_shadow_entry<<<(unsigned)std::min<int64_t>((n + 127) / 128, (int64_t)h->sm_count * 64), 128>>>(
+        sc.blockers, sc.em, glo, cell, g, P, h->shent, n);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());         // (renders may run on a non-blocking stream)
+    sc.shent = h->shent;
+    sc.shent_g = g;
+    sc.shent_p = P;
+    h->shent_ver = h->geo_ver;
+    return HRT_OK;
+}
+
 path::Camera to_cam(const hrt_camera& c) {
     path::Camera k{};
     std::memcpy(k.rot, c.rot, sizeof(k.rot));
@@ -1269,6 +1354,10 @@ int hrt_create(const hrt_scene_desc* d, hrt_handle** out) {
         if ((rc = build_occupancy(h, d->field.occ_threshold))) return bail(rc);
     }
     if ((rc = h->alloc((size_t)kTimedLaunches * 16, reinterpret_cast<void**>(&h->round_rows)))) return bail(rc);
+    {
+        const char* e = std::getenv("HRT_SHADOW_ENTRY");
+        h->shent_on = !(e && e[0] == '0');
+    }
     CK(cudaDeviceSynchronize());
     *out = h;
     return HRT_OK;
@@ -1336,6 +1425,7 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
     const int64_t chunk_pix = std::max<int64_t>(1, kMaxPaths / spp);
     int rc;
     if ((rc = ensure_state(h, std::min<int64_t>(total_pix, chunk_pix) * spp))) return rc;
+    if ((rc = ensure_shadow_entry(h))) return rc;
     CK(cudaMemsetAsync(h->ps.counters, 0, 64 * 4, st));
     CK(cudaMemsetAsync(h->ps.stats, 0, S_COUNT * 8, st));
     h->n_timed = 0;
@@ -1408,8 +1498,8 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
         stats->batch_rows = h->batch_rows + (int64_t)tot[S_ROWS];
         h->n_round_rows = std::min<int32_t>(ctr[C_RIDX], kTimedLaunches);
 #ifdef HRT_COUNT_STEPS
-        fprintf(stderr, "shadow trace: node steps %llu  triangle tests %llu  blocked %llu  queued %s\n",
-                tot[5], tot[6], tot[7], "");
+        fprintf(stderr, "shadow trace: cast %llu traced %llu blocked %llu | steps %llu, of blocked rays %llu\n",
+                tot[S_SHADOW], tot[9], tot[7], tot[5], tot[6]);
 #endif
     }
     if (ctr[C_NONFINITE] != 0) return fail(HRT_ENONFINITE, "non-finite or negative radiance in frame");
@@ -1432,6 +1522,7 @@ int hrt_transport(hrt_handle* h, const hrt_camera* cams, int32_t n_poses, int32_
     const int64_t chunk_pix = std::max<int64_t>(1, kMaxPaths / spp);
     int rc;
     if ((rc = ensure_state(h, std::min<int64_t>(npix, chunk_pix) * spp))) return rc;
+    if ((rc = ensure_shadow_entry(h))) return rc;
     const int64_t nrec = std::min<int64_t>(npix, chunk_pix) * spp * max_depth;
     int32_t* rface = nullptr;
     double* rval = nullptr;
@@ -1486,6 +1577,7 @@ int hrt_trace_paths(hrt_handle* h, const double* o, const double* d, const int64
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     int rc;
     if ((rc = ensure_state(h, n))) return rc;
+    if ((rc = ensure_shadow_entry(h))) return rc;
     CK(cudaMemsetAsync(h->ps.counters, 0, 64 * 4, st));
     CK(cudaMemsetAsync(h->ps.stats, 0, S_COUNT * 8, st));
     kern::Args a{};
@@ -1888,6 +1980,7 @@ int hrt_set_field_transform(hrt_handle* h, int32_t identity, const double* field
         for (int i = 0; i < 12; ++i) f.inv[i] = field_from_world[i];
     }
     f.identity = identity ? 1 : 0;       // (the occupancy grid lives in the field frame: unchanged)
+    ++h->geo_ver;                        // (the shadow entry table's grid covers the field box)
     return HRT_OK;
 }
 

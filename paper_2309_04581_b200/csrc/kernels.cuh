@@ -1001,6 +1001,25 @@ __global__ void __launch_bounds__(HRT_STEP_THREADS, HRT_STEP_MINB * 256 / HRT_ST
     if ((threadIdx.x & 31) == 0 && any) atomicAdd(&a.ps.counters[C_NS], any);
 }
 
+// Start node of a queued shadow ray from the shadow entry table
+// (bvh::k_shadow_entry): -2 = no blocker can be hit, 0 = the root (table off,
+// or x outside the table's grid).
+HRT_DEV int32_t shadow_start(const DevScene& sc, d3 x, const path::ShadowRay& r) {
+    if (!sc.shent) return 0;
+    const int32_t g = sc.shent_g, P = sc.shent_p;
+    const double f[3] = {(x.x - sc.shent_lo[0]) * sc.shent_inv[0], (x.y - sc.shent_lo[1]) * sc.shent_inv[1],
+                         (x.z - sc.shent_lo[2]) * sc.shent_inv[2]};
+    int32_t c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (!(f[a] >= 0.0 && f[a] < (double)g)) return 0;
+        c[a] = (int32_t)f[a];
+    }
+    const int32_t pu = min((int32_t)(r.su * P), P - 1), pv = min((int32_t)(r.u2 * P), P - 1);
+    const int64_t cell = (int64_t)c[0] + (int64_t)g * (c[1] + (int64_t)g * c[2]);
+    return __ldg(sc.shent + ((cell * sc.em.n + r.idx) * P + pv) * P + pu);
+}
+
 // K3 over the batch: one thread per sample row (sample-major, so a warp
 // traces the shadow rays of 32 neighbouring pixels at the same step). Rows
 // that cannot contribute (opacity 0 or black) cast no ray, as in the
@@ -1050,13 +1069,16 @@ __global__ void __launch_bounds__(256, HRT_SHADOW_MINB) k_shadow(Args a, MarchSt
             if (m.shq) {
                 // queue the ray for k_shadow_trace unless it misses the blocker tree's root
                 const path::ShadowRay r = path::shadow_ray_h(a.sc, x, m.h4[p], k);
-                if (bvh::root_overlap(a.sc.blockers, x, r.dir, a.sc.spawn_eps, r.tmax)) {
+                const int32_t start = shadow_start(a.sc, x, r);
+                if (start == -2) {
+                    code = 0;                          // no blocker can be hit (entry table)
+                } else if (bvh::root_overlap(a.sc.blockers, x, r.dir, a.sc.spawn_eps, r.tmax)) {
                     QRay q;
                     q.ox = x.x; q.oy = x.y; q.oz = x.z;
                     q.dx = r.dir.x; q.dy = r.dir.y; q.dz = r.dir.z;
                     q.tmax = r.tmax;
                     q.row = (int32_t)row;
-                    q.idx = r.idx;
+                    q.idx = a.sc.shent ? (r.idx | (start << 8)) : r.idx;   // (start node, emitter)
                     const int32_t qs = reserve(&a.ps.counters[C_SHQ]);
                     HRT_CHECK_ROW(m, qs);
                     m.shq[qs] = q;
@@ -1105,7 +1127,7 @@ __global__ void __launch_bounds__(256, HRT_SHTRACE_MINB) k_shadow_trace(Args a, 
     int sp = 0;
     int32_t cur = 0, row = 0, idx = 0;
 #ifdef HRT_COUNT_STEPS
-    long long n_steps = 0, n_mt = 0, n_blocked = 0;
+    long long n_steps = 0, n_mt = 0, n_blocked = 0, n_traced = 0, my_steps = 0;
 #endif
     while (true) {
         const bool idle = qi < 0 && !exhausted;
@@ -1124,12 +1146,12 @@ __global__ void __launch_bounds__(256, HRT_SHTRACE_MINB) k_shadow_trace(Args a, 
                     d = mk(q.dx, q.dy, q.dz);
                     tmax = q.tmax;
                     row = q.row;
-                    idx = q.idx;
+                    idx = a.sc.shent ? (q.idx & 255) : q.idx;
                     r32 = bvh::prep32(o, d);
                     t0 = bvh::t_lo32(t_min);
                     t1 = bvh::t_hi32(tmax);
                     sp = 0;
-                    cur = 0;
+                    cur = a.sc.shent ? (q.idx >> 8) : 0;    // the entry table's start node
                     qi = my;
                 } else {
                     exhausted = true;
@@ -1162,6 +1184,7 @@ __global__ void __launch_bounds__(256, HRT_SHTRACE_MINB) k_shadow_trace(Args a, 
             }
 #ifdef HRT_COUNT_STEPS
             ++n_steps;
+            ++my_steps;
 #endif
             if (!done) {
                 if (sp > 0) cur = stack[--sp];
@@ -1170,6 +1193,11 @@ __global__ void __launch_bounds__(256, HRT_SHTRACE_MINB) k_shadow_trace(Args a, 
             if (done) {
                 m.shadow[row] = blocked ? idx + 1 : 0;
                 qi = -1;
+#ifdef HRT_COUNT_STEPS
+                ++n_traced;
+                if (blocked) { ++n_blocked; n_mt += my_steps; }
+                my_steps = 0;
+#endif
             }
             continue;
         }
@@ -1214,6 +1242,7 @@ __global__ void __launch_bounds__(256, HRT_SHTRACE_MINB) k_shadow_trace(Args a, 
     stat_add(a.ps.stats, 5, n_steps);
     stat_add(a.ps.stats, 6, n_mt);
     stat_add(a.ps.stats, 7, n_blocked);
+    stat_add(a.ps.stats, 9, n_traced);
 #endif
 }
 

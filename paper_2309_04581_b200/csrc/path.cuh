@@ -97,6 +97,7 @@ struct ShadowRay {          // one shadow query: point p towards emitter idx, in
     d3 dir;
     double tmax;
     int32_t idx;
+    double su, u2;          // the light sample's (sqrt(u1), u2) (shadow entry table patch)
 };
 
 // EmitterSet.sample (render.py:96-107) + the ray set-up of shadow_mask_batch
@@ -125,6 +126,8 @@ HRT_DEV ShadowRay shadow_ray_h(const DevScene& sc, d3 p, uint64_t h4, int64_t la
     r.dir = {delta.x / safe, delta.y / safe, delta.z / safe};
     r.tmax = dist * (1.0 - 1e-4);
     r.idx = idx;
+    r.su = su;
+    r.u2 = u2;
     return r;
 }
 

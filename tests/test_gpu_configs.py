@@ -147,6 +147,58 @@ def test_shadowed_frame_pipelines_agree_at_scale(cuda):
         assert st["shadow_rays"] == stats[0]["shadow_rays"]
 
 
+def _render_entry(scene, on, spp, pixels=None):
+    """Render with the shadow entry table on or off (HRT_SHADOW_ENTRY is read at create)."""
+    import os
+    old = os.environ.get("HRT_SHADOW_ENTRY")
+    os.environ["HRT_SHADOW_ENTRY"] = "1" if on else "0"
+    try:
+        r = Renderer(scene)
+    finally:
+        if old is None:
+            del os.environ["HRT_SHADOW_ENTRY"]
+        else:
+            os.environ["HRT_SHADOW_ENTRY"] = old
+    img = r.render_pixels(scene.camera, spp, 3, pixels=pixels).cpu().numpy()
+    st = dict(r.last_stats)
+    r.close()
+    return img, st
+
+
+@pytest.mark.parametrize("moved", [False, True])
+def test_shadow_entry_table_exact(cuda, moved):
+    """Shadow rays started from the light-space entry table (the blocker-tree
+    node under which everything a ray from that field cell to that light
+    patch can hit lies, or no traversal at all) decide exactly what
+    traversals from the root decide: bit-identical images and equal sample
+    and shadow-ray counts, with the field box in place and moved (rotated +
+    shifted, so the table's grid covers a transformed box)."""
+    scene = shadow_scene()
+    scene.camera = Camera(configs.look_at_safe((0.0, 0.3, 4.0)), math.radians(40.0), (160, 120))
+    if moved:
+        scene.field.world_from_field = Transform.translate((0.15, -0.1, 0.05)).compose(
+            Transform.rotate((0.3, 1.0, 0.2), 0.4))
+    on, st_on = _render_entry(scene, True, 8)
+    off, st_off = _render_entry(scene, False, 8)
+    assert st_on["shadow_rays"] > 100_000
+    assert st_on["nerf_samples"] == st_off["nerf_samples"]
+    assert st_on["shadow_rays"] == st_off["shadow_rays"]
+    assert np.array_equal(on, off)
+
+
+def test_shadow_entry_table_exact_cfg4_geometry(cuda):
+    """The same on the full cfg4 blockers (300k-triangle displaced torus,
+    deep tree) with a small field: a 48 x 48 x 16 spp crop under the torus."""
+    scene = configs.cfg4(field=small_field(seed=11, act="softplus", F=4), res=(480, 270))
+    w, h = scene.camera.resolution
+    pix = torch.as_tensor(crop(w, h, 48, cx=240, cy=120).astype(np.int32), device=cuda)
+    on, st_on = _render_entry(scene, True, 16, pix)
+    off, st_off = _render_entry(scene, False, 16, pix)
+    assert st_on["shadow_rays"] > 100_000
+    assert st_on["shadow_rays"] == st_off["shadow_rays"]
+    assert np.array_equal(on, off)
+
+
 def test_gpu_cfg2_lambertian_crop(cuda):
     """cfg2: diffuse plane + 50k-triangle blob lit only by the NeRF, 16 spp
     stratified. The GPU reuses the reference RNG streams, so paths match the
