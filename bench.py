@@ -734,8 +734,9 @@ def run_ours(args, rank, world, local):
                 "requests_per_sample": req_per_sample,
                 "sectors_per_sample": traffic.get("l2_sectors_per_sample"),
                 "random_sector_gbs": l2["gather_sector_gbs"],
-                "peak_source": f"hrt_gather_peak (live, this run): independent random {entry_bytes}-B gathers over the "
-                               f"same table, {gather_gbs or 0:.0f} GB/s useful = 1 request each; requests/sample from "
+                "peak_source": f"hrt_gather_peak (live, this run): independent random {entry_bytes}-B gathers over an "
+                               f"L2-resident window (<= 64 MiB) of the same table, {gather_gbs or 0:.0f} GB/s useful = "
+                               "1 request each; requests/sample from "
                                f"{traffic_src} (ncu lts__t_requests_srcunit_tex_op_read over every field-engine "
                                f"launch of one frame, commit {traffic.get('commit')})",
             },

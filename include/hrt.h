@@ -242,8 +242,9 @@ int hrt_ipc_open(const uint8_t* handle64, void** ptr);
 int hrt_ipc_close(void* ptr);
 
 /* Roofline probe of the hash-grid encode: useful GB/s of independent random
- * one-entry gathers (8 B for F = 2, 16 B for F = 4) over this scene's hash
- * table, through the LSU path (mode 0), the TEX path (1) or both at once (2). */
+ * one-entry gathers (8 B for F = 2, 16 B for F = 4) over an L2-resident window
+ * (the first <= 64 MiB) of this scene's hash table, through the LSU path
+ * (mode 0), the TEX path (1) or both at once (2): the L1-miss request ceiling. */
 int hrt_gather_peak(hrt_handle* h, int32_t mode, double* gbs);
 
 /* Move the field (reference: a dynamic field object's world_from_field is

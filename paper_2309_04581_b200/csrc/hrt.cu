@@ -1892,7 +1892,9 @@ int hrt_gather_peak(hrt_handle* h, int32_t mode, double* gbs) {
         return fail(HRT_EINVAL, "needs a neural field (F = 2 or 4)");
     if (mode < 0 || mode > 2) return fail(HRT_EINVAL, "mode: 0 LSU, 1 TEX, 2 both");
     const NeuralField& nf = h->sc.field.nf;
-    const uint32_t n = (uint32_t)h->tab_entries;
+    // an L2-resident window (<= 64 MiB) of the table: the probe measures the L1-miss request
+    // ceiling to L2, not DRAM (cfg4's 344 MiB table would make it a DRAM random-read probe)
+    const uint32_t n = (uint32_t)std::min<int64_t>(h->tab_entries, (int64_t(64) << 20) / (4 * h->F));
     float* sink = nullptr;
     CK(cudaMalloc(&sink, 4));
     const int threads = 512, blocks = h->sm_count * 4, iters = 64;
