@@ -1203,7 +1203,7 @@ constexpr int32_t kShentGrid = HRT_SHENT_G;
 int ensure_shadow_entry(hrt_handle* h) {
     DevScene& sc = h->sc;
     const bool want = h->shent_on && HRT_BVH_WIDTH == 4 && sc.em.n > 0 && sc.em.n <= 16 &&
-                      sc.blockers.n_faces > 0 && sc.field.kind != HRT_FIELD_NONE &&
+                      sc.blockers.n_faces > 0 && sc.field.kind == HRT_FIELD_NEURAL &&   // (queued shadow rays)
                       h->rfb.n_q < (1 << 23);
     if (!want) {
         sc.shent = nullptr;
