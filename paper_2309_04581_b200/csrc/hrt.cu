@@ -1248,6 +1248,7 @@ int ensure_shadow_entry(hrt_handle* h) {
         sc.shent_inv[ax] = inv[ax];
     }
     const int64_t n = (int64_t)g * g * g * sc.em.n * P * P;
+    sc.shent = nullptr;                  // (until the new table is complete)
     if (n > h->shent_n) {
         if (h->shent) cudaFree(h->shent);
         h->shent = nullptr;
