@@ -315,25 +315,35 @@ HRT_DEV bool any_hit_w(const DevBvh& b, d3 o, d3 d, double t_min, double t_max) 
 }
 
 // ---------------------------------------------------- 4-wide traversal
-// The node's lo boxes and refs come through the LSU path, its hi boxes
-// through the TEX path (a float4 texture over the same array, same bits), so
-// divergent traversals spread their node fetches over both L1TEX data pipes
-// (round-1 ncu of the shadow tracer: LSU data pipe 84 % busy; measured:
-// shadow stage -4 %, closest hit +4 %, so only any-hit traversals use it).
+// Any-hit traversals fetch the node's refs and lo.x box row through the LSU
+// path and the other five box rows through the TEX path (a float4 texture
+// over the same array, same bits), so divergent traversals spread their node
+// fetches over both L1TEX data pipes (round-1 ncu of the shadow tracer: LSU
+// data pipe 84 % busy; hi rows on TEX: shadow stage -4 %; round 2, session 2:
+// lo.y and lo.z on TEX too, with LSU still at 73 %: cfg4 shadow stage
+// 664 -> 641 ms; all six: 650 ms). Closest-hit traversals keep LSU only
+// (+4 % with the split).
 #ifndef HRT_QNODE_TEX
 #define HRT_QNODE_TEX 1
+#endif
+#ifndef HRT_QNODE_TEX_FIELDS
+#define HRT_QNODE_TEX_FIELDS 5      // box float4s (from the end: hiz, hiy, hix, loz, loy, lox) fetched through TEX
 #endif
 template <bool kTex = false>
 HRT_DEV QNode load_q(const DevBvh& b, int32_t i) {
     const float4* p = reinterpret_cast<const float4*>(b.qnodes + i);
     QNode q;
-    q.lox = __ldg(p); q.loy = __ldg(p + 1); q.loz = __ldg(p + 2);
     if (kTex && HRT_QNODE_TEX && b.qtex) {
         const int t = 8 * i;
-        q.hix = tex1Dfetch<float4>(b.qtex, t + 3);
-        q.hiy = tex1Dfetch<float4>(b.qtex, t + 4);
-        q.hiz = tex1Dfetch<float4>(b.qtex, t + 5);
+        constexpr int NT = HRT_QNODE_TEX_FIELDS;
+        q.lox = NT >= 6 ? tex1Dfetch<float4>(b.qtex, t) : __ldg(p);
+        q.loy = NT >= 5 ? tex1Dfetch<float4>(b.qtex, t + 1) : __ldg(p + 1);
+        q.loz = NT >= 4 ? tex1Dfetch<float4>(b.qtex, t + 2) : __ldg(p + 2);
+        q.hix = NT >= 3 ? tex1Dfetch<float4>(b.qtex, t + 3) : __ldg(p + 3);
+        q.hiy = NT >= 2 ? tex1Dfetch<float4>(b.qtex, t + 4) : __ldg(p + 4);
+        q.hiz = NT >= 1 ? tex1Dfetch<float4>(b.qtex, t + 5) : __ldg(p + 5);
     } else {
+        q.lox = __ldg(p); q.loy = __ldg(p + 1); q.loz = __ldg(p + 2);
         q.hix = __ldg(p + 3); q.hiy = __ldg(p + 4); q.hiz = __ldg(p + 5);
     }
     q.ref = __ldg(reinterpret_cast<const int4*>(p + 6));
