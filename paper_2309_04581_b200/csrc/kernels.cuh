@@ -1054,17 +1054,21 @@ __global__ void __launch_bounds__(256, HRT_SHADOW_MINB) k_shadow(Args a, MarchSt
             li = (int64_t)((uint32_t)l - jj * S) * rm.width + jj;
         }
         const int64_t row = fws::phys_row(rm, li);
+        // the row's loads are issued together, then the path's (one latency each,
+        // not a chain; a hole row's output and k are read but unused)
         const int32_t p = m.in[row].path;
-        if (p < 0) continue;
         const float4 f = m.out[row];
-        const double rgb[3] = {(double)f.y, (double)f.z, (double)f.w};
+        const int32_t k = m.sk[row];
+        if (p < 0) continue;
         const double delta = m.delta[p];
+        const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
+        const double s0 = m.s0[p];
+        const int32_t nseg = m.n[p];
+        const double rgb[3] = {(double)f.y, (double)f.z, (double)f.w};
         const double al = 1.0 - exp(-(double)f.x * delta);
         int32_t code = 0;
         if (needs_shadow(a.sc, al, rgb)) {
-            const d3 o = mk(s.ox[p], s.oy[p], s.oz[p]), d = mk(s.dx[p], s.dy[p], s.dz[p]);
-            const Segment g{m.s0[p], delta, m.n[p]};
-            const int32_t k = m.sk[row];
+            const Segment g{s0, delta, nseg};
             const d3 x = sample_point(o, d, g, k);
             if (m.shq) {
                 // queue the ray for k_shadow_trace unless it misses the blocker tree's root
