@@ -59,6 +59,12 @@ constexpr int64_t kBatchCap = int64_t(1) << HRT_BATCH_CAP_LOG2;   // samples per
 #define HRT_TEX_LEVELS 8
 #endif
 constexpr int kTexLevels = HRT_TEX_LEVELS;        // finest levels gathered via TEX
+#ifndef HRT_TEAM_TEX_LEVELS
+#define HRT_TEAM_TEX_LEVELS 12
+#endif
+// ... in the encode-team (coherent) rounds of an F = 2 field: 10-16 TEX levels there
+// measured equal and 2 ms faster per cfg3 frame than 8 (F = 4: 8 stays best)
+constexpr int kTeamTexLevels = HRT_TEAM_TEX_LEVELS;
 #ifndef HRT_TEAM_ROUNDS
 #define HRT_TEAM_ROUNDS 3
 #endif
@@ -705,7 +711,9 @@ int launch_ws(hrt_handle* h, const fws::SampleIn* in, fws::RowMap rm, int64_t n,
     const int64_t tiles = (n + fws::kRows - 1) / fws::kRows;
     const int grid = round_ctr ? h->sm_count
                                : (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)h->sm_count));
-    fws::k_field_ws<E, F, T><<<grid, fws::kThreads, smem, st>>>(h->sc.field.nf, in, rm, n, dir32, out,
+    NeuralField nf = h->sc.field.nf;
+    if (T == 2 && F == 2) nf.tex_from = std::max(0, nf.n_levels - kTeamTexLevels);
+    fws::k_field_ws<E, F, T><<<grid, fws::kThreads, smem, st>>>(nf, in, rm, n, dir32, out,
                                                              density_only, round_ctr, h->ps.stats,
                                                              round_ctr ? h->round_rows : nullptr);
     CK(cudaGetLastError());
