@@ -298,9 +298,12 @@ HRT_DEV int32_t dda_next(const NeuralField& nf, const DevField& f, d3 of, d3 df,
 // The evaluated sample set and the compositing order equal the oracle's
 // per-sample march (oracle/tracer.py march), so parity is unchanged.
 #ifndef HRT_ROUND_SAMPLES
-#define HRT_ROUND_SAMPLES 32
+#define HRT_ROUND_SAMPLES 24
 #endif
-constexpr int kRoundSamples = HRT_ROUND_SAMPLES;   // max midpoints per path per round
+// max midpoints per path per round (cfg3 frame 16 / 20 / 24 / 28 / 32 / 40: 197.1 / 195.8 /
+// 196.5 / 198.3 / 199.9 / 201.2 ms; cfg1 14.0 / 13.8 / 13.4 / 13.3 / 13.4 / 13.4 ms; 24 also
+// the fastest at every 1-8-GPU rank share of cfg3)
+constexpr int kRoundSamples = HRT_ROUND_SAMPLES;
 #ifndef HRT_ROUND_SAMPLES_SMALL
 #define HRT_ROUND_SAMPLES_SMALL 48
 #endif
