@@ -51,8 +51,11 @@ constexpr int kIoChunks = 4;                       // pieces of the e2e frame re
 #define HRT_SHADOW_QUEUE 1
 #endif
 constexpr bool kShadowQueue = HRT_SHADOW_QUEUE;   // shadow rays: set-up pass + persistent tracer
+// Batch rows per march round: 2^27 lets a full 2^22-path chunk take up to 32 samples per
+// path in its first rounds (2^26 capped them at 16): cfg3 frame 196.5 -> 195.8 ms, cfg4
+// 960x540x64 1314 -> 1309 ms (chunks of 2^23 paths: cfg3 194.2 ms but cfg4 1357 ms)
 #ifndef HRT_BATCH_CAP_LOG2
-#define HRT_BATCH_CAP_LOG2 26
+#define HRT_BATCH_CAP_LOG2 27
 #endif
 constexpr int64_t kBatchCap = int64_t(1) << HRT_BATCH_CAP_LOG2;   // samples per march round
 #ifndef HRT_TEX_LEVELS
