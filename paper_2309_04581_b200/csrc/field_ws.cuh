@@ -252,9 +252,9 @@ k_field_ws(NeuralField nf, const SampleIn* __restrict__ in, RowMap rmap, int64_t
                     // gathers - what the MLP pipeline sustains when it is fed
 #pragma unroll
                     for (int k = 0; k < NL * F; ++k) v[k] = 0.01f * (float)k * rel.x - rel.y;
-                } else if constexpr (NL % (T == 2 ? 1 : kInflightF<F>) == 0) {
+                } else if constexpr (NL % (T >= 2 ? 1 : kInflightF<F>) == 0) {
                     // kInflightF levels of gathers in flight per thread (1 with two teams)
-                    constexpr int IF = T == 2 ? 1 : kInflightF<F>;
+                    constexpr int IF = T >= 2 ? 1 : kInflightF<F>;
 #pragma unroll
                     for (int j = 0; j < NL; j += IF) {
                         nerf::LevelLoadsF<F> g[IF];

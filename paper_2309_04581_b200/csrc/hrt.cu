@@ -71,7 +71,11 @@ constexpr int kTeamTexLevels = HRT_TEAM_TEX_LEVELS;
 #ifndef HRT_TEAM_ROUNDS
 #define HRT_TEAM_ROUNDS 3
 #endif
-constexpr int kTeamRounds = HRT_TEAM_ROUNDS;       // march rounds run with two encode teams (fws T = 2)
+constexpr int kTeamRounds = HRT_TEAM_ROUNDS;       // march rounds run with encode teams (fws T >= 2)
+#ifndef HRT_TEAMS_F2
+#define HRT_TEAMS_F2 2
+#endif
+constexpr int kTeamsF2 = HRT_TEAMS_F2;            // encode teams in the E = 32, F = 2 team rounds
 #ifndef HRT_TEAM_ROUNDS_F4
 #define HRT_TEAM_ROUNDS_F4 5
 #endif
@@ -715,7 +719,7 @@ int launch_ws(hrt_handle* h, const fws::SampleIn* in, fws::RowMap rm, int64_t n,
     const int grid = round_ctr ? h->sm_count
                                : (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)h->sm_count));
     NeuralField nf = h->sc.field.nf;
-    if (T == 2 && F == 2) nf.tex_from = std::max(0, nf.n_levels - kTeamTexLevels);
+    if (T >= 2 && F == 2) nf.tex_from = std::max(0, nf.n_levels - kTeamTexLevels);
     fws::k_field_ws<E, F, T><<<grid, fws::kThreads, smem, st>>>(nf, in, rm, n, dir32, out,
                                                              density_only, round_ctr, h->ps.stats,
                                                              round_ctr ? h->round_rows : nullptr);
@@ -739,7 +743,7 @@ int field_ws(hrt_handle* h, const fws::SampleIn* in, fws::RowMap rm, int64_t n, 
                        : launch_ws<16, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st);
             break;
         case 32 * 8 + 2:
-            rc = teams ? launch_ws<32, 2, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st)
+            rc = teams ? launch_ws<32, 2, kTeamsF2>(h, in, rm, n, dir32, out, density_only, round_ctr, st)
                        : launch_ws<32, 2>(h, in, rm, n, dir32, out, density_only, round_ctr, st);
             break;
         case 64 * 8 + 4:
