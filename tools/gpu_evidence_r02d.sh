@@ -5,7 +5,7 @@
 # bench lines then read), the cfg3 / cfg4 bench lines, the reference arm, the 2-rank flow,
 # the bench's launch list, per-round rows, full ncu captures and the scale probe.
 set -x
-O=gpurun_out/ev4
+O=${O:-gpurun_out/ev4}
 mkdir -p $O
 C=$(cat .commit 2>/dev/null)
 nvidia-smi > $O/nvsmi.txt 2>&1
