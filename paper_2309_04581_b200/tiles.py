@@ -52,9 +52,16 @@ class FrameGather:
             pad[q, :len(ids)] = ids
         self.row_pixel = torch.as_tensor(pad.reshape(-1), device=device)
 
+    def _collective(self):
+        # the all-gather runs whenever a process group exists (a 1-rank NCCL group
+        # too, so the collective path is exercised on a one-GPU box); without one
+        # (plain single process) the local buffer is the frame
+        import torch.distributed as dist
+        return self.world > 1 or (dist.is_available() and dist.is_initialized())
+
     def gather(self):
         import torch.distributed as dist
-        if self.world > 1:
+        if self._collective():
             dist.all_gather(self.parts, self.local, group=self.group)
             parts = self.parts
         else:
@@ -71,7 +78,7 @@ class FrameGather:
         (rank 0) or None."""
         import torch
         import torch.distributed as dist
-        if self.world > 1:
+        if self._collective():
             dist.all_gather(self.parts, self.local, group=self.group)
             rows = torch.cat(self.parts)
         else:
