@@ -37,9 +37,13 @@ int fail(int code, const std::string& msg) {
     } while (0)
 
 #ifndef HRT_MAX_PATHS_LOG2
-#define HRT_MAX_PATHS_LOG2 22
+#define HRT_MAX_PATHS_LOG2 23
 #endif
 constexpr int64_t kMaxPaths = int64_t(1) << HRT_MAX_PATHS_LOG2;   // paths per wavefront chunk
+// ... except for F = 4 fields (cfg4): 2^23-path chunks measured 1357 vs 1309 ms per
+// 960x540x64 frame there, while cfg3 gains from them (193.8 vs 195.3 ms: two chunks of
+// tail rounds and k_paths launches instead of four)
+constexpr int64_t kMaxPathsF4 = std::min<int64_t>(kMaxPaths, int64_t(1) << 22);
 constexpr int kThreads = 256;
 #ifndef HRT_STEP_THREADS
 #define HRT_STEP_THREADS 128
@@ -53,7 +57,7 @@ constexpr int kIoChunks = 4;                       // pieces of the e2e frame re
 constexpr bool kShadowQueue = HRT_SHADOW_QUEUE;   // shadow rays: set-up pass + persistent tracer
 // Batch rows per march round: 2^27 lets a full 2^22-path chunk take up to 32 samples per
 // path in its first rounds (2^26 capped them at 16): cfg3 frame 196.5 -> 195.8 ms, cfg4
-// 960x540x64 1314 -> 1309 ms (chunks of 2^23 paths: cfg3 194.2 ms but cfg4 1357 ms)
+// 960x540x64 1314 -> 1309 ms; a 2^23-path chunk (F = 2) takes up to 16 in its first rounds
 #ifndef HRT_BATCH_CAP_LOG2
 #define HRT_BATCH_CAP_LOG2 27
 #endif
@@ -1438,7 +1442,7 @@ int hrt_render(hrt_handle* h, const hrt_camera* cam, int32_t spp, uint64_t seed,
         return HRT_OK;
     }
     if (!out) return fail(HRT_EINVAL, "null argument");
-    const int64_t chunk_pix = std::max<int64_t>(1, kMaxPaths / spp);
+    const int64_t chunk_pix = std::max<int64_t>(1, (h->F == 4 ? kMaxPathsF4 : kMaxPaths) / spp);
     int rc;
     if ((rc = ensure_state(h, std::min<int64_t>(total_pix, chunk_pix) * spp))) return rc;
     if ((rc = ensure_shadow_entry(h))) return rc;

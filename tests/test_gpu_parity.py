@@ -333,20 +333,20 @@ def test_empty_pixel_list(cuda):
 
 @pytest.mark.parametrize("continuous", [True, False])
 def test_multi_chunk_frame_equals_single_chunks(cuda, continuous):
-    """A call with more paths than one wavefront chunk (2^22) is rendered
+    """A call with more paths than one wavefront chunk (2^23 for this F = 2 field) is rendered
     as several chunks back to back (new rays, queues and march rounds per
     chunk); every pixel must come out as when it is rendered in a call of
     its own that fits one chunk (paths are keyed by pixel and sample)."""
     scene = configs.cfg0()
     r = Renderer(scene)
     r.set_march(continuous)
-    spp = 1100                                   # 4096 px x 1100 spp = 4.5 M paths: 2 chunks
+    spp = 2100                                   # 4096 px x 2100 spp = 8.6 M paths: 2 chunks
     w, h = scene.camera.resolution
     full = r.render_pixels(scene.camera, spp, 2).cpu().numpy()
     samples_full = r.last_stats["nerf_samples"]
     assert r.last_stats["paths"] == w * h * spp
     parts, samples = [], 0
-    for lo in range(0, w * h, 1024):             # 1024 px x 1100 spp = 1.1 M paths: 1 chunk
+    for lo in range(0, w * h, 1024):             # 1024 px x 2100 spp = 2.2 M paths: 1 chunk
         pix = torch.arange(lo, lo + 1024, dtype=torch.int32, device=cuda)
         parts.append(r.render_pixels(scene.camera, spp, 2, pixels=pix).cpu().numpy())
         samples += r.last_stats["nerf_samples"]
